@@ -1,0 +1,186 @@
+/*
+ * expmc_b200 — C ABI of the B200-native Monte Carlo exp(tA)v hot path.
+ *
+ * Drop-in boundary for the reference C++ API (namespace expmc,
+ * /root/reference/proj/include/expmc/estimator.hpp:59-72 and
+ * sparse_matrix.hpp:105).  Plain pointers and sizes only; no CUDA or torch
+ * types.  Every function returns an expmc_status; on failure
+ * expmc_cuda_last_error() (thread-local) holds the message, which for
+ * argument errors is the reference's own std::invalid_argument text.
+ *
+ * Conventions (mirroring the reference):
+ *   - NodeId is uint32_t (sparse_matrix.hpp:11).
+ *   - The matrix is immutable after creation and may be shared by callers
+ *     (sparse_matrix.hpp:63-65); a handle is bound to one CUDA device and
+ *     should be used by one host thread at a time.
+ *   - Host-buffer calls are synchronous and blocking, like the reference.
+ *   - *_device calls take device pointers on the handle's device and a
+ *     cudaStream_t passed as void* (NULL = the handle's own stream); they
+ *     are asynchronous on that stream.
+ */
+#ifndef EXPMC_B200_H_
+#define EXPMC_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    EXPMC_OK = 0,
+    EXPMC_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+    EXPMC_RUNTIME_ERROR = 2,    /* reference: std::runtime_error     */
+    EXPMC_CUDA_ERROR = 3        /* CUDA failure (maps to runtime_error) */
+} expmc_status;
+
+/* Splitting (estimator.hpp:11). */
+enum { EXPMC_LIE = 0, EXPMC_STRANG = 1 };
+
+/* Walker engine.  PHILOX is the production path (K3/K4: continuous clock,
+ * counter-based RNG keyed by (seed, row, walker)).  PCG_COMPAT (K2) replays
+ * the reference's PCG32 streams path by path for parity checks. */
+enum { EXPMC_RNG_PHILOX = 0, EXPMC_RNG_PCG_COMPAT = 1 };
+
+/* PathParams (estimator.hpp:16-33): dt = beta / n_steps. */
+typedef struct {
+    double beta;
+    uint64_t n_steps;
+    uint64_t samples;  /* M: walkers per entry (entry) or in total (vector, tc) */
+    int32_t splitting; /* EXPMC_LIE or EXPMC_STRANG */
+    int32_t rng;       /* EXPMC_RNG_PHILOX or EXPMC_RNG_PCG_COMPAT */
+    uint64_t seed;
+} expmc_path_params;
+
+/* Estimate (estimator.hpp:37-42). */
+typedef struct {
+    double value;
+    double std_error;
+    uint64_t samples_used;
+    uint64_t total_jumps;
+} expmc_estimate;
+
+typedef struct expmc_matrix expmc_matrix; /* device-resident SplitMatrix */
+
+const char* expmc_cuda_last_error(void);
+int expmc_cuda_abi_version(void); /* 1 */
+
+/* ------------------------------------------------------------ matrices */
+/* From the mirrored adjacency of a SparseSymmetric (sparse_matrix.hpp:25-61):
+ * rows sorted by column, both directions stored, off-diagonal weights > 0,
+ * diagonal separately (diag may be NULL = zero).  Validated on the device
+ * with from_entries' checks (sparse_matrix.cpp:20-51), then split() runs on
+ * the device (K1, bit-exact with sparse_matrix.cpp:101-142). */
+int expmc_cuda_create_from_csr(uint64_t n, const uint64_t* row_ptr, const uint32_t* col,
+                               const double* val, const double* diag, int device,
+                               expmc_matrix** out);
+/* From an existing reference SplitMatrix (sparse_matrix.hpp:66-91): its
+ * row_offset / neighbor / weight / diag fields.  rate, cum, d, uniform_row,
+ * dbar and dmax are re-derived on the device bit-exactly. */
+int expmc_cuda_create_from_split(uint64_t n, const uint64_t* row_offset,
+                                 const uint32_t* neighbor, const double* weight,
+                                 const double* diag, int device, expmc_matrix** out);
+int expmc_cuda_destroy(expmc_matrix* m);
+
+int expmc_cuda_matrix_info(const expmc_matrix* m, uint64_t* n, uint64_t* nnz, double* dbar,
+                           uint64_t* dmax, int32_t* any_nonuniform, int32_t* device);
+/* Copy the device SplitMatrix back (any pointer may be NULL). */
+int expmc_cuda_split_export(const expmc_matrix* m, double* diag, double* d, double* rate,
+                            uint64_t* row_offset, uint32_t* neighbor, double* weight,
+                            double* cum, uint8_t* uniform_row);
+/* Walker alias tables (nnz each): keep column k of a row when a u32 coin is
+ * < thr[k], else jump to column alias[k].  Uniform rows hold thr = ~0. */
+int expmc_cuda_alias_export(const expmc_matrix* m, uint32_t* thr, uint32_t* alias);
+/* Packed 32-byte row records {u32 off, u32 deg|nonuniform<<31, f32 1/rate,
+ * u32 0, f64 d, f64 v}, n * 32 bytes. */
+int expmc_cuda_records_export(const expmc_matrix* m, void* out);
+
+/* ---------------------------------------------------------- estimators */
+/* entry_estimate (estimator.cpp:169-206): one entry i of
+ * the splitting approximation to exp(beta A) v. */
+int expmc_cuda_entry_estimate(expmc_matrix* m, const double* v, uint64_t nv, uint32_t i,
+                              const expmc_path_params* p, expmc_estimate* out);
+/* Batched entry_estimate over rows[0..nrows) (rows == NULL: every row,
+ * nrows must equal n): the "full vector with W walkers per entry". */
+int expmc_cuda_entries(expmc_matrix* m, const double* v, uint64_t nv, const uint32_t* rows,
+                       uint64_t nrows, const expmc_path_params* p, double* value,
+                       double* std_error, uint64_t* jumps);
+/* vector_estimate (estimator.cpp:208-278), Theorem 2; values has n entries. */
+int expmc_cuda_vector_estimate(expmc_matrix* m, const double* v, uint64_t nv,
+                               const expmc_path_params* p, double* values,
+                               double* std_error_global, uint64_t* total_jumps,
+                               double* v_sum);
+/* tc_estimate (estimator.cpp:280-318). */
+int expmc_cuda_tc_estimate(expmc_matrix* m, const expmc_path_params* p, expmc_estimate* out);
+
+/* -------------------------------------------- device-resident variants */
+/* Stage v (device pointer, n doubles) for subsequent *_device calls:
+ * checks finiteness (same message as check_vector) and packs v into the
+ * row records.  Synchronises the stream to report errors. */
+int expmc_cuda_set_v_device(expmc_matrix* m, const double* v_dev, uint64_t nv, void* stream);
+/* Philox entry walker (K3) over device rows -> device outputs, async.
+ * Rows are NOT range-checked here (the caller's host layer does that). */
+int expmc_cuda_entries_device(expmc_matrix* m, const uint32_t* rows_dev, uint64_t nrows,
+                              const expmc_path_params* p, double* value_dev,
+                              double* std_error_dev, uint64_t* jumps_dev, void* stream);
+/* K6 gather ceiling: chains_per_row chains of chain_len jumps from every
+ * listed row (memory-only walker, same access pattern as K3), async. */
+int expmc_cuda_gather_ceiling_device(expmc_matrix* m, const uint32_t* rows_dev, uint64_t nrows,
+                                     uint32_t chains_per_row, uint32_t chain_len, void* stream);
+/* Lane slots T per entry used by the Philox entry walker for W walkers:
+ * walker l runs in slot l mod T, slots are summed sequentially, then by a
+ * fixed xor tree per warp and in warp order — part of the result contract
+ * (oracle/fast_model.c replays it). */
+uint32_t expmc_cuda_entry_slots(uint64_t walkers);
+/* Number of kernels this library has launched in this process. */
+uint64_t expmc_cuda_launch_count(void);
+
+/* ------------------------------------------------------- accuracy (K5) */
+/* Deterministic fp64 y = exp(t A) v by scaled Taylor series (tol relative). */
+int expmc_cuda_expmv(expmc_matrix* m, const double* v, uint64_t nv, double t, double tol,
+                     double* out);
+/* stats() power iteration (sparse_matrix.cpp:176-217) on the device:
+ * largest eigenvalue of A via the Gershgorin-shifted power method. */
+int expmc_cuda_lambda_max(expmc_matrix* m, uint64_t power_iters, double* lambda_max,
+                          double* rel_change);
+/* Deterministic splitting product the estimators sample:
+ *   Strang (e^{dt D/2} e^{-dt L} e^{dt D/2})^N v,  Lie (e^{-dt L} e^{dt D})^N v. */
+int expmc_cuda_splitting_product(expmc_matrix* m, const double* v, uint64_t nv,
+                                 const expmc_path_params* p, double tol, double* out);
+
+/* ----------------------------------------- synthetic inputs (host, C++) */
+/* Host CSR builders for the benchmark configurations.  The returned object
+ * owns a mirrored, row-sorted CSR (the SparseSymmetric adjacency) plus the
+ * diagonal. */
+typedef struct expmc_csr expmc_csr;
+const char* expmc_gen_last_error(void); /* message of the last failed expmc_gen_* */
+/* 2-D 5-point / 3-D 7-point Dirichlet FD stencil scaled by s:
+ * diag -2*dim*s, neighbours +s. */
+int expmc_gen_fd(int dim, uint64_t side, double s, expmc_csr** out);
+/* Barabasi-Albert exactly as generate({ScaleFree, n, m0, seed})
+ * (generators.cpp:58-103). */
+int expmc_gen_ba(uint64_t n, uint64_t m0, uint64_t seed, expmc_csr** out);
+/* Watts-Strogatz: ring with k/2 neighbours per side, each edge rewired with
+ * probability p (no self loops, no duplicates), PCG32 stream (seed, 0). */
+int expmc_gen_ws(uint64_t n, uint64_t half_k, double p, uint64_t seed, expmc_csr** out);
+int expmc_csr_sizes(const expmc_csr* c, uint64_t* n, uint64_t* nnz);
+int expmc_csr_export(const expmc_csr* c, uint64_t* row_ptr, uint32_t* col, double* val,
+                     double* diag);
+/* Zero-copy views (valid until expmc_csr_free). */
+int expmc_csr_view(const expmc_csr* c, const uint64_t** row_ptr, const uint32_t** col,
+                   const double** val, const double** diag);
+void expmc_csr_free(expmc_csr* c);
+/* Seeded vectors / row samples with PCG32 RngStream(seed, 0):
+ *   kind 0: U[0,1)  1: U[-1,1)  2: 3-D Gaussian bump (sigma) + U[0,1) on a
+ *   side^3 grid (row-major, cube [0,1]^3, centre 0.5) */
+int expmc_gen_vector(int kind, uint64_t n, uint64_t side, double sigma, uint64_t seed,
+                     double* out);
+/* k distinct rows of [0, n), uniform without replacement (partial
+ * Fisher-Yates, RngStream(seed, 0)), returned sorted ascending. */
+int expmc_gen_row_sample(uint64_t n, uint64_t k, uint64_t seed, uint32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EXPMC_B200_H_ */

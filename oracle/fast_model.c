@@ -1,0 +1,194 @@
+/*
+ * TEST INFRASTRUCTURE ONLY — a CPU model of the B200 production walker
+ * (K3 entry_fast_kernel, paper_1904_12759_b200/csrc/walk_fast.cu), written
+ * independently from the kernel's contract so the GPU can be pinned walker
+ * for walker, not only statistically.
+ *
+ * The law it samples is the reference's (entry_estimate, Theorem 1:
+ * proj/src/estimator.cpp:169-206 with run_path :26-39 and advance
+ * sampler.cpp:36-49), with the two re-formulations the kernel makes:
+ *   - one exponential clock per sojourn instead of one per Δt segment
+ *     (memorylessness), crediting d_s to each grid point kΔt
+ *     covered by the sojourn (half weight at k = 0 and k = N for Strang);
+ *   - Philox4x32-10 keyed by the seed, counter (step, walker, row, 'ENTR').
+ * That this law matches the reference is checked statistically against
+ * oracle/_ref (tests/test_oracle.py); that the GPU matches this model is
+ * checked per entry (tests/test_gpu_parity.py).
+ *
+ * Build with -ffp-contract=off: every float/double operation below is a
+ * single IEEE operation, exactly like the __*_rn intrinsics of the kernel.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+    uint32_t off, degf;
+    float inv_rate;
+    uint32_t spare;
+    double d, v;
+} fm_rec;
+
+#define FM_NONUNIFORM 0x80000000u
+#define FM_DEGMASK 0x7fffffffu
+#define FM_TAG_ENTRY 0x454e5452u
+
+void fm_philox(const uint32_t ctr[4], uint32_t k0, uint32_t k1, uint32_t out[4]) {
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+float fm_neg_ln_u(uint32_t w) {
+    const float u = ((float)(w >> 9) + 0.5f) * 0x1.0p-23f;
+    uint32_t bits;
+    memcpy(&bits, &u, 4);
+    int e = (int)((bits >> 23) & 0xffu) - 127;
+    const uint32_t mb = (bits & 0x007fffffu) | 0x3f800000u;
+    float m;
+    memcpy(&m, &mb, 4);
+    if (m > 1.41421356f) {
+        m = m * 0.5f;
+        e += 1;
+    }
+    const float s = (m - 1.0f) / (m + 1.0f);
+    const float z = s * s;
+    float p = fmaf(z, 0.11111111f, 0.14285715f);
+    p = fmaf(z, p, 0.2f);
+    p = fmaf(z, p, 0.33333334f);
+    p = fmaf(z, p, 1.0f);
+    const float lnm = (2.0f * s) * p;
+    const float ln_u = fmaf((float)e, 0.693147182f, lnm);
+    return -ln_u;
+}
+
+static uint32_t fm_pick(uint32_t hi, uint32_t lo, uint32_t n) {
+    const uint64_t x = ((uint64_t)hi << 32) | lo;
+    return (uint32_t)(((unsigned __int128)x * n) >> 64);
+}
+
+/* Records as split_pack builds them (csrc/split_pack.cu). */
+void fm_build_records(uint64_t n, const uint64_t* row_ptr, const double* rate,
+                      const double* d, const uint8_t* uniform_row, const double* v,
+                      fm_rec* rec) {
+    for (uint64_t i = 0; i < n; ++i) {
+        rec[i].off = (uint32_t)row_ptr[i];
+        rec[i].degf = (uint32_t)(row_ptr[i + 1] - row_ptr[i]) |
+                      (uniform_row[i] ? 0u : FM_NONUNIFORM);
+        rec[i].inv_rate = (float)(1.0 / rate[i]);
+        rec[i].spare = 0;
+        rec[i].d = d[i];
+        rec[i].v = v[i];
+    }
+}
+
+/* One row: per-slot sequential sums over walkers l = slot, slot+T, ...;
+ * xor-butterfly within each warp; warps summed in index order. */
+void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
+                const uint32_t* thr, const uint32_t* alias, const uint32_t* rows,
+                uint64_t nrows, double beta, uint64_t N, uint64_t W, int strang,
+                uint64_t seed, uint32_t T, double* value, double* se,
+                uint64_t* jumps) {
+    const double dt = beta / (double)N;
+    const double inv_dt = 1.0 / dt;
+    const double n_grid = (double)N;
+    const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    double* a1 = (double*)malloc(sizeof(double) * T);
+    double* a2 = (double*)malloc(sizeof(double) * T);
+    uint64_t* aj = (uint64_t*)malloc(sizeof(uint64_t) * T);
+    double b1[32], b2[32];
+    uint64_t bj[32];
+    for (uint64_t r = 0; r < nrows; ++r) {
+        const uint32_t i = rows[r];
+        const fm_rec ri = rec[i];
+        const double p0 = exp(-(rate[i] * beta));
+        const uint64_t T0 = (uint64_t)(p0 * 4294967296.0);
+        const double f0 = exp(beta * ri.d) * ri.v;
+        const double corr_i = strang ? 0.5 * ri.d : ri.d;
+        for (uint32_t slot = 0; slot < T; ++slot) {
+            double s1 = 0.0, s2 = 0.0;
+            uint64_t jt = 0;
+            for (uint64_t l = slot; l < W; l += T) {
+                fm_rec cur = ri;
+                double t = 0.0, S = 0.0;
+                uint32_t g = 0, step = 0, jc = 0;
+                for (;;) {
+                    const uint32_t ctr[4] = {step, (uint32_t)l, i, FM_TAG_ENTRY};
+                    uint32_t w[4];
+                    fm_philox(ctr, k0, k1, w);
+                    if (step == 0 && (uint64_t)w[0] < T0) break; /* never jumps */
+                    const float h = fm_neg_ln_u(w[0]) * cur.inv_rate;
+                    const double tn = t + (double)h * inv_dt;
+                    if (tn >= n_grid) {
+                        S = fma(cur.d, (double)(N + 1 - g), S);
+                        const double corr = strang ? corr_i + 0.5 * cur.d : corr_i;
+                        const double f = exp(dt * (S - corr)) * cur.v;
+                        const double dev = f - f0;
+                        s1 = s1 + dev;
+                        s2 = fma(dev, dev, s2);
+                        jt += jc;
+                        break;
+                    }
+                    const uint32_t kk = (uint32_t)ceil(tn);
+                    S = fma(cur.d, (double)(kk - g), S);
+                    g = kk;
+                    t = tn;
+                    const uint32_t deg = cur.degf & FM_DEGMASK;
+                    uint32_t k = fm_pick(w[1], w[3], deg);
+                    if (cur.degf & FM_NONUNIFORM) {
+                        if (w[2] >= thr[cur.off + k]) k = alias[cur.off + k];
+                    }
+                    cur = rec[nbr[cur.off + k]];
+                    ++jc;
+                    ++step;
+                }
+            }
+            a1[slot] = s1;
+            a2[slot] = s2;
+            aj[slot] = jt;
+        }
+        /* butterfly per warp */
+        double w1 = 0.0, w2 = 0.0;
+        uint64_t wj = 0;
+        for (uint32_t wbase = 0; wbase < T; wbase += 32) {
+            for (int q = 0; q < 32; ++q) { b1[q] = a1[wbase + q]; b2[q] = a2[wbase + q]; bj[q] = aj[wbase + q]; }
+            for (int o = 16; o > 0; o >>= 1) {
+                double c1[32], c2[32];
+                uint64_t cj[32];
+                for (int q = 0; q < 32; ++q) {
+                    c1[q] = b1[q] + b1[q ^ o];
+                    c2[q] = b2[q] + b2[q ^ o];
+                    cj[q] = bj[q] + bj[q ^ o];
+                }
+                memcpy(b1, c1, sizeof(c1));
+                memcpy(b2, c2, sizeof(c2));
+                memcpy(bj, cj, sizeof(cj));
+            }
+            if (wbase == 0) { w1 = b1[0]; w2 = b2[0]; wj = bj[0]; }
+            else { w1 = w1 + b1[0]; w2 = w2 + b2[0]; wj += bj[0]; }
+        }
+        const double Wd = (double)W;
+        value[r] = f0 + w1 / Wd;
+        double sev = 0.0;
+        if (W > 1) {
+            double var = (w2 - (w1 * w1) / Wd) / (Wd - 1.0);
+            if (var < 0.0) var = 0.0;
+            sev = sqrt(var / Wd);
+        }
+        se[r] = sev;
+        jumps[r] = wj;
+    }
+    free(a1);
+    free(a2);
+    free(aj);
+}

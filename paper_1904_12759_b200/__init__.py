@@ -1,0 +1,23 @@
+"""paper_1904_12759_b200 — B200-native Monte Carlo exp(tA)v hot path.
+
+The reference's estimator API (arXiv 1904.12759 C++ artifact,
+/root/reference/proj/include/expmc/estimator.hpp) over a C ABI
+(include/expmc_b200.h) implemented by hand-written sm_100a kernels in
+``csrc/``.  There is no CPU fallback: every estimate runs on the GPU.
+"""
+from ._lib import ExpmcError, lib
+from .estimator import (EntriesEstimate, Estimate, PathParams, Rng, SplitMatrix, Splitting,
+                        VectorEstimate, entries_device, entries_estimate, entry_estimate,
+                        entry_slots, expmv, gather_ceiling_device, launch_count, set_v_device,
+                        split, splitting_product, tc_estimate, vector_estimate)
+from .inputs import Csr, build_config, csr_from_dense, gen_ba, gen_fd, gen_row_sample, gen_vector, gen_ws, n_rule
+from .spectral import BetaRule, lambda_max, resolve_beta
+
+__all__ = [
+    "ExpmcError", "lib", "EntriesEstimate", "Estimate", "PathParams", "Rng", "SplitMatrix",
+    "Splitting", "VectorEstimate", "entries_device", "entries_estimate", "entry_estimate",
+    "entry_slots", "expmv", "gather_ceiling_device", "launch_count", "set_v_device", "split",
+    "splitting_product", "tc_estimate", "vector_estimate", "Csr", "build_config",
+    "csr_from_dense", "gen_ba", "gen_fd", "gen_row_sample", "gen_vector", "gen_ws", "n_rule",
+    "BetaRule", "lambda_max", "resolve_beta",
+]

@@ -1,0 +1,790 @@
+// Host driver behind the C ABI (include/expmc_b200.h).
+//
+// Mirrors the reference's estimator entry points and their argument
+// validation (proj/src/estimator.cpp:130-139, :161-173, :210-222, :283) with
+// the same std::invalid_argument messages, then launches the sm_100a
+// kernels.  No CPU fallback exists: every estimate is computed on the GPU.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "expmc_b200.h"
+#include "kernels.cuh"
+
+using namespace expmc_b200;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+struct InvalidArg : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct CudaErr : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                         \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess)                                                        \
+            throw CudaErr(std::string(#x) + ": " + cudaGetErrorString(e_));           \
+    } while (0)
+
+void after_launch(uint64_t kernels) {
+    g_launches += kernels;
+    CK(cudaGetLastError());
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return EXPMC_OK;
+    } catch (const CudaErr& e) {
+        g_err = e.what();
+        return EXPMC_CUDA_ERROR;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return EXPMC_INVALID_ARGUMENT;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return EXPMC_RUNTIME_ERROR;
+    } catch (...) {
+        g_err = "unknown error";
+        return EXPMC_RUNTIME_ERROR;
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        CK(cudaGetDevice(&prev));
+        if (prev != dev) CK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// grow-only device scratch buffer
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    template <class T>
+    T* get(size_t count) {
+        const size_t bytes = count * sizeof(T) ? count * sizeof(T) : 16;
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            CK(cudaMalloc(&p, bytes));
+            cap = bytes;
+        }
+        return static_cast<T*>(p);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+std::string pair_str(uint64_t a, uint64_t b) {
+    if (a > b) std::swap(a, b);  // reference prints the canonical upper triangle
+    return "(" + std::to_string(a) + ", " + std::to_string(b) + ")";
+}
+
+void validate_params(const expmc_path_params* p) {
+    // PathParams::validate, estimator.cpp:161-167
+    if (!p) throw InvalidArg("PathParams pointer is null");
+    if (!(p->beta > 0.0) || !std::isfinite(p->beta))
+        throw InvalidArg("beta must be positive and finite");
+    if (p->n_steps == 0) throw InvalidArg("n_steps must be >= 1");
+    if (p->samples == 0) throw InvalidArg("samples must be >= 1");
+    if (p->splitting != EXPMC_LIE && p->splitting != EXPMC_STRANG)
+        throw InvalidArg("unknown splitting");
+    if (p->rng != EXPMC_RNG_PHILOX && p->rng != EXPMC_RNG_PCG_COMPAT)
+        throw InvalidArg("unknown rng engine");
+    if (p->rng == EXPMC_RNG_PHILOX && p->n_steps >= (1ull << 31))
+        throw InvalidArg("n_steps must be < 2^31 for the continuous-clock walker");
+}
+
+FastParams fast_params(const expmc_path_params* p, uint64_t walkers) {
+    FastParams f;
+    f.beta = p->beta;
+    f.dt = p->beta / (double)p->n_steps;  // PathParams::dt, estimator.hpp:27
+    f.inv_dt = 1.0 / f.dt;
+    f.n_grid = (double)p->n_steps;
+    f.N = (uint32_t)p->n_steps;
+    f.strang = p->splitting == EXPMC_STRANG;
+    f.W = walkers;
+    f.k0 = (uint32_t)p->seed;
+    f.k1 = (uint32_t)(p->seed >> 32);
+    return f;
+}
+
+}  // namespace
+
+struct expmc_matrix {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DevSplit m;
+    std::vector<void*> owned;
+    DevBuf vdev, rows, out_val, out_se, out_j, fa, vcum, values, pa, pb, pc, scal, tmp1, tmp2,
+        tmp3, iota;
+    uint64_t iota_n = 0;
+    // host copies kept for K5 norm bounds
+    std::vector<double> h_rate, h_diag;
+
+    template <class T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        CK(cudaMalloc(&p, (count ? count : 1) * sizeof(T)));
+        owned.push_back(p);
+        return static_cast<T*>(p);
+    }
+    ~expmc_matrix() {
+        for (void* p : owned) cudaFree(p);
+        for (DevBuf* b : {&vdev, &rows, &out_val, &out_se, &out_j, &fa, &vcum, &values, &pa,
+                          &pb, &pc, &scal, &tmp1, &tmp2, &tmp3, &iota})
+            b->release();
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+cudaStream_t pick_stream(expmc_matrix* h, void* s) {
+    return s ? static_cast<cudaStream_t>(s) : h->stream;
+}
+
+void check_vector(const expmc_matrix* h, const double* v, uint64_t nv) {
+    // check_vector, estimator.cpp:130-139
+    if (nv != h->m.n || (!v && nv)) throw InvalidArg("vector length does not match matrix");
+    for (uint64_t k = 0; k < nv; ++k)
+        if (!std::isfinite(v[k])) throw InvalidArg("non-finite entry in v");
+}
+
+const uint32_t* all_rows(expmc_matrix* h) {
+    uint32_t* d = h->iota.get<uint32_t>(h->m.n);
+    if (h->iota_n != h->m.n) {
+        std::vector<uint32_t> tmp(h->m.n);
+        for (uint64_t k = 0; k < h->m.n; ++k) tmp[k] = (uint32_t)k;
+        CK(cudaMemcpy(d, tmp.data(), h->m.n * 4, cudaMemcpyHostToDevice));
+        h->iota_n = h->m.n;
+    }
+    return d;
+}
+
+expmc_matrix* build(uint64_t n, const uint64_t* row_ptr, const uint32_t* col, const double* val,
+                    const double* diag, int device) {
+    if (n >= (1ull << 32)) throw InvalidArg("n must be < 2^32 (NodeId is 32-bit)");
+    if (n && !row_ptr) throw InvalidArg("row_ptr is null");
+    if (n && row_ptr[0] != 0) throw InvalidArg("row_ptr[0] must be 0");
+    for (uint64_t i = 0; i < n; ++i)
+        if (row_ptr[i + 1] < row_ptr[i]) throw InvalidArg("row_ptr must be non-decreasing");
+    const uint64_t nnz = n ? row_ptr[n] : 0;
+    if (nnz >= (1ull << 32)) throw InvalidArg("nnz must be < 2^32");
+    if (nnz && (!col || !val)) throw InvalidArg("col / val is null");
+    if (diag)
+        for (uint64_t i = 0; i < n; ++i)
+            if (!std::isfinite(diag[i]))
+                throw InvalidArg("non-finite weight at " + pair_str(i, i));
+
+    DeviceGuard g(device);
+    auto* h = new expmc_matrix;
+    try {
+        h->device = device;
+        CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        DevSplit& m = h->m;
+        m.n = n;
+        m.nnz = nnz;
+        m.diag = h->alloc<double>(n);
+        m.d = h->alloc<double>(n);
+        m.rate = h->alloc<double>(n);
+        m.row_offset = h->alloc<uint64_t>(n + 1);
+        m.neighbor = h->alloc<uint32_t>(nnz);
+        m.weight = h->alloc<double>(nnz);
+        m.cum = h->alloc<double>(nnz);
+        m.uniform_row = h->alloc<uint8_t>(n);
+        m.rec = h->alloc<RowRec>(n);
+        cudaStream_t s = h->stream;
+        if (n) {
+            CK(cudaMemcpyAsync(m.row_offset, row_ptr, (n + 1) * 8, cudaMemcpyHostToDevice, s));
+            if (diag)
+                CK(cudaMemcpyAsync(m.diag, diag, n * 8, cudaMemcpyHostToDevice, s));
+            else
+                CK(cudaMemsetAsync(m.diag, 0, n * 8, s));
+        }
+        if (nnz) {
+            CK(cudaMemcpyAsync(m.neighbor, col, nnz * 4, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(m.weight, val, nnz * 8, cudaMemcpyHostToDevice, s));
+        }
+        // small device scalars: [0] err key, [1] dmax, [2] any_nonuniform
+        unsigned long long* sc = h->scal.get<unsigned long long>(4);
+        const unsigned long long init[4] = {~0ull, 0ull, 0ull, 0ull};
+        CK(cudaMemcpyAsync(sc, init, sizeof(init), cudaMemcpyHostToDevice, s));
+        launch_validate_csr(n, m.row_offset, m.neighbor, m.weight, sc, s);
+        after_launch(n ? 1 : 0);
+        unsigned long long res[4];
+        CK(cudaMemcpyAsync(res, sc, sizeof(res), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (res[0] != ~0ull) {
+            const uint64_t i = res[0] >> 24;
+            const int kind = (int)((res[0] >> 20) & 0xf);
+            const uint64_t k = row_ptr[i] + (res[0] & 0xfffff);
+            const uint64_t j = col[k];
+            switch (kind) {  // messages of from_entries, sparse_matrix.cpp:20-51
+                case 1:
+                    throw InvalidArg("entry " + pair_str(i, j) + " out of range for n = " +
+                                     std::to_string(n));
+                case 2: throw InvalidArg("non-finite weight at " + pair_str(i, j));
+                case 3: throw InvalidArg("explicit zero entry at " + pair_str(i, j));
+                case 4:
+                    throw InvalidArg("negative off-diagonal weight at " + pair_str(i, j) +
+                                     ": no CTMC interpretation");
+                case 5:
+                    if (k > row_ptr[i] && col[k - 1] == j)
+                        throw InvalidArg("duplicate entry at " + pair_str(i, j));
+                    throw InvalidArg("CSR row " + std::to_string(i) + " is not sorted by column");
+                case 6:
+                    throw InvalidArg("diagonal entry at " + pair_str(i, i) +
+                                     " stored in the adjacency; pass it in diag");
+                default:
+                    throw InvalidArg("matrix is not symmetric at " + pair_str(i, j));
+            }
+        }
+        launch_split_pack(n, m.row_offset, m.weight, m.diag, m.d, m.rate, m.cum,
+                          m.uniform_row, m.rec, sc + 1, reinterpret_cast<unsigned int*>(sc + 2),
+                          s);
+        after_launch(n ? 1 : 0);
+        CK(cudaMemcpyAsync(res, sc, sizeof(res), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        m.dmax = res[1];
+        m.any_nonuniform = (res[2] & 0xffffffffull) != 0;
+        m.dbar = n > 0 ? (double)nnz / (double)n : 0.0;  // sparse_matrix.cpp:138-141
+        if (m.any_nonuniform) {
+            m.alias_thr = h->alloc<uint32_t>(nnz);
+            m.alias_idx = h->alloc<uint32_t>(nnz);
+            double* p = h->tmp1.get<double>(nnz);
+            uint32_t* sm = h->tmp2.get<uint32_t>(nnz);
+            uint32_t* lg = h->tmp3.get<uint32_t>(nnz);
+            launch_alias_build(n, m.row_offset, m.weight, m.rate, m.uniform_row, m.alias_thr,
+                               m.alias_idx, p, sm, lg, s);
+            after_launch(1);
+            CK(cudaStreamSynchronize(s));
+            h->tmp1.release();
+            h->tmp2.release();
+            h->tmp3.release();
+        }
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    return h;
+}
+
+// Run the entry estimator for host rows / host v; outputs to host.
+void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* rows,
+                 uint64_t nrows, const expmc_path_params* p, double* value, double* se,
+                 uint64_t* jumps) {
+    validate_params(p);
+    check_vector(h, v, nv);
+    const uint64_t n = h->m.n;
+    if (rows) {
+        for (uint64_t r = 0; r < nrows; ++r)
+            if (rows[r] >= n) throw InvalidArg("entry index out of range");
+    } else if (nrows != n) {
+        throw InvalidArg("rows == NULL requires nrows == n");
+    }
+    if (p->rng == EXPMC_RNG_PHILOX && p->samples >= (1ull << 32))
+        throw InvalidArg("samples must be < 2^32 for the entry walker");
+    if (nrows == 0) return;
+    DeviceGuard g(h->device);
+    cudaStream_t s = h->stream;
+    double* vd = h->vdev.get<double>(n);
+    CK(cudaMemcpyAsync(vd, v, n * 8, cudaMemcpyHostToDevice, s));
+    const uint32_t* rd;
+    if (rows) {
+        uint32_t* r = h->rows.get<uint32_t>(nrows);
+        CK(cudaMemcpyAsync(r, rows, nrows * 4, cudaMemcpyHostToDevice, s));
+        rd = r;
+    } else {
+        rd = all_rows(h);
+    }
+    double* ov = h->out_val.get<double>(nrows);
+    double* os = h->out_se.get<double>(nrows);
+    uint64_t* oj = h->out_j.get<uint64_t>(nrows);
+    if (p->rng == EXPMC_RNG_PHILOX) {
+        launch_pack_v(n, vd, h->m.rec, s);
+        launch_entry_fast(h->m, rd, nrows, fast_params(p, p->samples), ov, os, oj, s);
+        after_launch(2);
+    } else {
+        const double dt = p->beta / (double)p->n_steps;
+        const bool strang = p->splitting == EXPMC_STRANG;
+        double* f = h->fa.get<double>(n);
+        launch_node_factors(n, h->m.d, strang ? dt / 2.0 : dt, f, s);
+        launch_entry_compat(h->m, vd, rd, nrows, dt, p->n_steps, p->samples,
+                            strang ? f : nullptr, f, p->seed, ov, os, oj, s);
+        after_launch(2);
+    }
+    CK(cudaMemcpyAsync(value, ov, nrows * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(se, os, nrows * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(jumps, oj, nrows * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+}
+
+// Theorem 2 walkers (vector / tc).  start_mode 0 uniform, 1 categorical.
+void run_scatter(expmc_matrix* h, int start_mode, const std::vector<double>* cum, double v_sum,
+                 const expmc_path_params* p, double* values_host, double* sum_out,
+                 double* sq_out, uint64_t* jumps_out) {
+    DeviceGuard g(h->device);
+    cudaStream_t s = h->stream;
+    const uint64_t n = h->m.n;
+    double* vals = nullptr;
+    if (values_host) {
+        vals = h->values.get<double>(n);
+        CK(cudaMemsetAsync(vals, 0, n * 8, s));
+    }
+    const double* vc = nullptr;
+    if (start_mode == 1) {
+        double* c = h->vcum.get<double>(n);
+        CK(cudaMemcpyAsync(c, cum->data(), n * 8, cudaMemcpyHostToDevice, s));
+        vc = c;
+    }
+    const unsigned parts =
+        p->rng == EXPMC_RNG_PHILOX ? scatter_fast_grid() : scatter_compat_grid();
+    double* pa = h->pa.get<double>(parts);
+    double* pb = h->pb.get<double>(parts);
+    unsigned long long* pc = h->pc.get<unsigned long long>(parts);
+    if (p->rng == EXPMC_RNG_PHILOX) {
+        launch_scatter_fast(h->m, start_mode, vc, v_sum, fast_params(p, p->samples), vals, pa,
+                            pb, pc, s);
+    } else {
+        const double dt = p->beta / (double)p->n_steps;
+        const bool strang = p->splitting == EXPMC_STRANG;
+        double* f = h->fa.get<double>(n);
+        launch_node_factors(n, h->m.d, strang ? dt / 2.0 : dt, f, s);
+        after_launch(1);
+        // Lie weight on the state each segment leaves from (estimator.cpp:228-231)
+        launch_scatter_compat(h->m, start_mode, vc, v_sum, dt, p->n_steps, p->samples, f,
+                              strang ? f : nullptr, p->seed, vals, pa, pb, pc, s);
+    }
+    after_launch(1);
+    double* tot = h->scal.get<double>(4);
+    launch_final_reduce(pa, pb, pc, parts, tot, tot + 1,
+                        reinterpret_cast<unsigned long long*>(tot + 2), s);
+    after_launch(1);
+    if (vals) {
+        launch_scale(n, vals, 1.0 / (double)p->samples, s);
+        after_launch(1);
+        CK(cudaMemcpyAsync(values_host, vals, n * 8, cudaMemcpyDeviceToHost, s));
+    }
+    double res[3];
+    CK(cudaMemcpyAsync(res, tot, sizeof(res), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *sum_out = res[0];
+    *sq_out = res[1];
+    std::memcpy(jumps_out, &res[2], 8);
+}
+
+void finalize(double sum, double sum_sq, uint64_t ms, double* value, double* se) {
+    // estimator.cpp:76-89
+    const double mm = (double)ms;
+    *value = sum / mm;
+    *se = 0.0;
+    if (ms > 1) {
+        const double var = std::max(0.0, (sum_sq - sum * sum / mm) / (mm - 1.0));
+        *se = std::sqrt(var / mm);
+    }
+}
+
+// y = exp(tau * (B + shift I)) x by Taylor on device buffers; B = A (mode 0)
+// or -L (mode 1).  x is overwritten with the result.
+void taylor_step(expmc_matrix* h, int mode, double shift, double tau, double tol, double* x,
+                 double* term, double* tmp, cudaStream_t s) {
+    const uint64_t n = h->m.n;
+    const unsigned parts = norm_parts();
+    double* part = h->pa.get<double>(parts);
+    std::vector<double> hp(parts);
+    auto norm = [&](const double* y) {
+        launch_norm_inf(n, y, part, parts, s);
+        after_launch(1);
+        CK(cudaMemcpyAsync(hp.data(), part, parts * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double m = 0.0;
+        for (double v : hp) m = std::max(m, v);
+        return m;
+    };
+    CK(cudaMemcpyAsync(term, x, n * 8, cudaMemcpyDeviceToDevice, s));
+    for (int k = 1; k <= 200; ++k) {
+        launch_spmv(h->m, mode, shift, term, tmp, s);
+        after_launch(1);
+        launch_scale(n, tmp, tau / (double)k, s);
+        after_launch(1);
+        std::swap(term, tmp);
+        launch_axpy(n, 1.0, term, x, s);
+        after_launch(1);
+        const double nt = norm(term);
+        if (nt <= tol * norm(x)) return;
+    }
+}
+
+// exp(t (B)) x with B = A (mode 0) or -L (mode 1), Gershgorin-shifted and
+// split into substeps of norm <= 2.
+void expmv_dev(expmc_matrix* h, int mode, double t, double tol, double* x, cudaStream_t s) {
+    const uint64_t n = h->m.n;
+    if (n == 0) return;
+    if (h->h_rate.size() != n) {
+        h->h_rate.resize(n);
+        h->h_diag.resize(n);
+        CK(cudaMemcpyAsync(h->h_rate.data(), h->m.rate, n * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(h->h_diag.data(), h->m.diag, n * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    double lo = INFINITY, hi = -INFINITY;
+    for (uint64_t i = 0; i < n; ++i) {
+        const double c = mode == 0 ? h->h_diag[i] : -h->h_rate[i];
+        lo = std::min(lo, c - h->h_rate[i]);
+        hi = std::max(hi, c + h->h_rate[i]);
+    }
+    const double mu = 0.5 * (lo + hi), rad = 0.5 * (hi - lo);
+    const uint64_t steps = std::max<uint64_t>(1, (uint64_t)std::ceil(std::fabs(t) * rad / 2.0));
+    const double tau = t / (double)steps;
+    double* term = h->tmp1.get<double>(n);
+    double* tmp = h->tmp2.get<double>(n);
+    for (uint64_t k = 0; k < steps; ++k) taylor_step(h, mode, -mu, tau, tol, x, term, tmp, s);
+    launch_scale(n, x, std::exp(t * mu), s);
+    after_launch(1);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* expmc_cuda_last_error(void) { return g_err.c_str(); }
+int expmc_cuda_abi_version(void) { return 1; }
+uint64_t expmc_cuda_launch_count(void) { return g_launches.load(); }
+uint32_t expmc_cuda_entry_slots(uint64_t walkers) {
+    return 32u * (uint32_t)entry_fast_wpr(walkers);
+}
+
+int expmc_cuda_create_from_csr(uint64_t n, const uint64_t* row_ptr, const uint32_t* col,
+                               const double* val, const double* diag, int device,
+                               expmc_matrix** out) {
+    return guarded([&] {
+        if (!out) throw InvalidArg("out is null");
+        *out = build(n, row_ptr, col, val, diag, device);
+    });
+}
+
+int expmc_cuda_create_from_split(uint64_t n, const uint64_t* row_offset,
+                                 const uint32_t* neighbor, const double* weight,
+                                 const double* diag, int device, expmc_matrix** out) {
+    return expmc_cuda_create_from_csr(n, row_offset, neighbor, weight, diag, device, out);
+}
+
+int expmc_cuda_destroy(expmc_matrix* m) {
+    return guarded([&] {
+        if (!m) return;
+        DeviceGuard g(m->device);
+        cudaStreamSynchronize(m->stream);
+        delete m;
+    });
+}
+
+int expmc_cuda_matrix_info(const expmc_matrix* h, uint64_t* n, uint64_t* nnz, double* dbar,
+                           uint64_t* dmax, int32_t* any_nonuniform, int32_t* device) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        if (n) *n = h->m.n;
+        if (nnz) *nnz = h->m.nnz;
+        if (dbar) *dbar = h->m.dbar;
+        if (dmax) *dmax = h->m.dmax;
+        if (any_nonuniform) *any_nonuniform = h->m.any_nonuniform ? 1 : 0;
+        if (device) *device = h->device;
+    });
+}
+
+int expmc_cuda_split_export(const expmc_matrix* h, double* diag, double* d, double* rate,
+                            uint64_t* row_offset, uint32_t* neighbor, double* weight,
+                            double* cum, uint8_t* uniform_row) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        DeviceGuard g(h->device);
+        const DevSplit& m = h->m;
+        auto cp = [&](void* dst, const void* src, size_t bytes) {
+            if (dst && bytes) CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+        };
+        cp(diag, m.diag, m.n * 8);
+        cp(d, m.d, m.n * 8);
+        cp(rate, m.rate, m.n * 8);
+        cp(row_offset, m.row_offset, (m.n + 1) * 8);
+        cp(neighbor, m.neighbor, m.nnz * 4);
+        cp(weight, m.weight, m.nnz * 8);
+        cp(cum, m.cum, m.nnz * 8);
+        cp(uniform_row, m.uniform_row, m.n);
+    });
+}
+
+int expmc_cuda_alias_export(const expmc_matrix* h, uint32_t* thr, uint32_t* alias) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        DeviceGuard g(h->device);
+        const DevSplit& m = h->m;
+        if (!m.any_nonuniform) {  // uniform everywhere: identity tables
+            std::vector<uint64_t> ro(m.n + 1);
+            if (m.n) CK(cudaMemcpy(ro.data(), m.row_offset, (m.n + 1) * 8, cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < m.n; ++i)
+                for (uint64_t k = ro[i]; k < ro[i + 1]; ++k) {
+                    if (thr) thr[k] = 0xffffffffu;
+                    if (alias) alias[k] = (uint32_t)(k - ro[i]);
+                }
+            return;
+        }
+        if (thr) CK(cudaMemcpy(thr, m.alias_thr, m.nnz * 4, cudaMemcpyDeviceToHost));
+        if (alias) CK(cudaMemcpy(alias, m.alias_idx, m.nnz * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+int expmc_cuda_records_export(const expmc_matrix* h, void* out) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        DeviceGuard g(h->device);
+        if (h->m.n) CK(cudaMemcpy(out, h->m.rec, h->m.n * sizeof(RowRec), cudaMemcpyDeviceToHost));
+    });
+}
+
+int expmc_cuda_entry_estimate(expmc_matrix* h, const double* v, uint64_t nv, uint32_t i,
+                              const expmc_path_params* p, expmc_estimate* out) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        validate_params(p);
+        check_vector(h, v, nv);
+        if (i >= h->m.n) throw InvalidArg("entry index out of range");
+        double val, se;
+        uint64_t j;
+        run_entries(h, v, nv, &i, 1, p, &val, &se, &j);
+        out->value = val;
+        out->std_error = se;
+        out->samples_used = p->samples;
+        out->total_jumps = j;
+    });
+}
+
+int expmc_cuda_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* rows,
+                       uint64_t nrows, const expmc_path_params* p, double* value,
+                       double* std_error, uint64_t* jumps) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        run_entries(h, v, nv, rows, nrows, p, value, std_error, jumps);
+    });
+}
+
+int expmc_cuda_vector_estimate(expmc_matrix* h, const double* v, uint64_t nv,
+                               const expmc_path_params* p, double* values,
+                               double* std_error_global, uint64_t* total_jumps,
+                               double* v_sum_out) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        validate_params(p);
+        check_vector(h, v, nv);
+        double v_sum = 0.0;  // estimator.cpp:212-222
+        for (uint64_t k = 0; k < nv; ++k) {
+            if (v[k] < 0.0) throw InvalidArg("vector_estimate requires v >= 0 entrywise");
+            v_sum += v[k];
+        }
+        if (!(v_sum > 0.0)) throw InvalidArg("vector_estimate requires sum(v) > 0");
+        // StartSampler (estimator.cpp:92-128): exact uniform test, else cum
+        bool uniform = true;
+        for (uint64_t k = 0; k < nv; ++k)
+            if (v[k] != v[0]) { uniform = false; break; }
+        std::vector<double> cum;
+        if (!uniform) {
+            cum.resize(nv);
+            double acc = 0.0;
+            for (uint64_t k = 0; k < nv; ++k) { acc += v[k]; cum[k] = acc; }
+        }
+        double sum, sq;
+        uint64_t j;
+        run_scatter(h, uniform ? 0 : 1, &cum, v_sum, p, values, &sum, &sq, &j);
+        double value;
+        finalize(sum, sq, p->samples, &value, std_error_global);
+        *total_jumps = j;
+        *v_sum_out = v_sum;
+    });
+}
+
+int expmc_cuda_tc_estimate(expmc_matrix* h, const expmc_path_params* p, expmc_estimate* out) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        validate_params(p);
+        if (h->m.n == 0) throw InvalidArg("empty matrix");  // estimator.cpp:283
+        double sum, sq;
+        uint64_t j;
+        run_scatter(h, 0, nullptr, (double)h->m.n, p, nullptr, &sum, &sq, &j);
+        finalize(sum, sq, p->samples, &out->value, &out->std_error);
+        out->samples_used = p->samples;
+        out->total_jumps = j;
+    });
+}
+
+int expmc_cuda_set_v_device(expmc_matrix* h, const double* v_dev, uint64_t nv, void* stream) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        if (nv != h->m.n) throw InvalidArg("vector length does not match matrix");
+        DeviceGuard g(h->device);
+        cudaStream_t s = pick_stream(h, stream);
+        unsigned int* flag = h->scal.get<unsigned int>(4);
+        CK(cudaMemsetAsync(flag, 0, 4, s));
+        launch_count_nonfinite(nv, v_dev, flag, s);
+        after_launch(1);
+        unsigned int bad = 0;
+        CK(cudaMemcpyAsync(&bad, flag, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (bad) throw InvalidArg("non-finite entry in v");
+        launch_pack_v(nv, v_dev, h->m.rec, s);
+        after_launch(1);
+    });
+}
+
+int expmc_cuda_entries_device(expmc_matrix* h, const uint32_t* rows_dev, uint64_t nrows,
+                              const expmc_path_params* p, double* value_dev,
+                              double* std_error_dev, uint64_t* jumps_dev, void* stream) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        validate_params(p);
+        if (p->rng != EXPMC_RNG_PHILOX)
+            throw InvalidArg("entries_device supports the Philox walker only");
+        if (p->samples >= (1ull << 32))
+            throw InvalidArg("samples must be < 2^32 for the entry walker");
+        DeviceGuard g(h->device);
+        launch_entry_fast(h->m, rows_dev, nrows, fast_params(p, p->samples), value_dev,
+                          std_error_dev, jumps_dev, pick_stream(h, stream));
+        after_launch(nrows ? 1 : 0);
+    });
+}
+
+int expmc_cuda_gather_ceiling_device(expmc_matrix* h, const uint32_t* rows_dev, uint64_t nrows,
+                                     uint32_t chains_per_row, uint32_t chain_len,
+                                     void* stream) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        DeviceGuard g(h->device);
+        unsigned long long* sink = h->scal.get<unsigned long long>(4);
+        launch_gather_ceiling(h->m, rows_dev, nrows, chains_per_row, chain_len, 0x2545F491u,
+                              sink, pick_stream(h, stream));
+        after_launch(1);
+    });
+}
+
+int expmc_cuda_expmv(expmc_matrix* h, const double* v, uint64_t nv, double t, double tol,
+                     double* out) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        check_vector(h, v, nv);
+        if (!std::isfinite(t)) throw InvalidArg("t must be finite");
+        if (!(tol > 0.0)) throw InvalidArg("tol must be positive");
+        DeviceGuard g(h->device);
+        cudaStream_t s = h->stream;
+        const uint64_t n = h->m.n;
+        double* x = h->tmp3.get<double>(n);
+        CK(cudaMemcpyAsync(x, v, n * 8, cudaMemcpyHostToDevice, s));
+        expmv_dev(h, 0, t, tol, x, s);
+        CK(cudaMemcpyAsync(out, x, n * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    });
+}
+
+int expmc_cuda_lambda_max(expmc_matrix* h, uint64_t power_iters, double* lambda_max,
+                          double* rel_change) {
+    // stats(): proj/src/sparse_matrix.cpp:176-217 (power iteration on A
+    // shifted by its Gershgorin lower bound), on the device.
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        const uint64_t n = h->m.n;
+        *lambda_max = 0.0;
+        if (rel_change) *rel_change = 0.0;
+        if (power_iters == 0 || n == 0) return;
+        DeviceGuard g(h->device);
+        cudaStream_t s = h->stream;
+        if (h->h_rate.size() != n) {
+            h->h_rate.resize(n);
+            h->h_diag.resize(n);
+            CK(cudaMemcpyAsync(h->h_rate.data(), h->m.rate, n * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(h->h_diag.data(), h->m.diag, n * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+        double shift = 0.0;
+        for (uint64_t i = 0; i < n; ++i) shift = std::max(shift, h->h_rate[i] - h->h_diag[i]);
+        double* x = h->tmp1.get<double>(n);
+        double* y = h->tmp2.get<double>(n);
+        std::vector<double> x0(n, 1.0 / std::sqrt((double)n));
+        CK(cudaMemcpyAsync(x, x0.data(), n * 8, cudaMemcpyHostToDevice, s));
+        const unsigned parts = norm_parts();
+        double* pa = h->pa.get<double>(parts);
+        double* pb = h->pb.get<double>(parts);
+        unsigned long long* pc = h->pc.get<unsigned long long>(parts);
+        double* tot = h->scal.get<double>(4);
+        double lambda = 0.0, prev = 0.0, rel = 0.0;
+        for (uint64_t it = 0; it < power_iters; ++it) {
+            launch_spmv(h->m, 0, shift, x, y, s);  // y = (A + shift I) x
+            launch_dot2(n, x, y, pa, pb, pc, parts, s);
+            launch_final_reduce(pa, pb, pc, parts, tot, tot + 1,
+                                reinterpret_cast<unsigned long long*>(tot + 2), s);
+            after_launch(3);
+            double res[2];
+            CK(cudaMemcpyAsync(res, tot, sizeof(res), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            prev = lambda;
+            lambda = res[0] - shift;
+            const double norm = std::sqrt(res[1]);
+            if (norm == 0.0) break;
+            CK(cudaMemcpyAsync(x, y, n * 8, cudaMemcpyDeviceToDevice, s));
+            launch_scale(n, x, 1.0 / norm, s);
+            after_launch(1);
+            if (it > 0) rel = std::fabs(lambda - prev) / std::max(std::fabs(lambda), 1e-300);
+        }
+        CK(cudaStreamSynchronize(s));
+        *lambda_max = lambda;
+        if (rel_change) *rel_change = rel;
+    });
+}
+
+int expmc_cuda_splitting_product(expmc_matrix* h, const double* v, uint64_t nv,
+                                 const expmc_path_params* p, double tol, double* out) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        validate_params(p);
+        check_vector(h, v, nv);
+        if (!(tol > 0.0)) throw InvalidArg("tol must be positive");
+        DeviceGuard g(h->device);
+        cudaStream_t s = h->stream;
+        const uint64_t n = h->m.n;
+        double* x = h->tmp3.get<double>(n);
+        CK(cudaMemcpyAsync(x, v, n * 8, cudaMemcpyHostToDevice, s));
+        const double dt = p->beta / (double)p->n_steps;
+        const bool strang = p->splitting == EXPMC_STRANG;
+        for (uint64_t k = 0; k < p->n_steps; ++k) {
+            launch_scale_diag(n, h->m.d, strang ? dt / 2.0 : dt, x, s);
+            after_launch(1);
+            expmv_dev(h, 1, dt, tol, x, s);
+            if (strang) {
+                launch_scale_diag(n, h->m.d, dt / 2.0, x, s);
+                after_launch(1);
+            }
+        }
+        CK(cudaMemcpyAsync(out, x, n * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+// Internal declarations shared by the .cu translation units and the host
+// driver (api.cu).  Not part of the public C ABI (include/expmc_b200.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace expmc_b200 {
+
+// Device-resident SplitMatrix (proj/include/expmc/sparse_matrix.hpp:66-91)
+// plus the B200 walk layout.  All pointers are device pointers.
+struct DevSplit {
+    uint64_t n = 0, nnz = 0;
+    // SplitMatrix fields, same meaning and bits as the reference
+    double* diag = nullptr;
+    double* d = nullptr;
+    double* rate = nullptr;
+    uint64_t* row_offset = nullptr;
+    uint32_t* neighbor = nullptr;
+    double* weight = nullptr;
+    double* cum = nullptr;
+    uint8_t* uniform_row = nullptr;
+    double dbar = 0.0;
+    uint64_t dmax = 0;
+    bool any_nonuniform = false;
+    // walk layout
+    RowRec* rec = nullptr;       // n packed 32-B row records
+    uint32_t* alias_thr = nullptr; // nnz (only if any_nonuniform)
+    uint32_t* alias_idx = nullptr; // nnz (only if any_nonuniform)
+};
+
+// Parameters of the fast walkers (K3/K4).  Built once on the host from
+// PathParams; the CPU model oracle/fast_model.c consumes the same numbers.
+struct FastParams {
+    double beta;   // horizon β
+    double dt;     // β / N
+    double inv_dt; // N / β
+    double n_grid; // (double) N
+    uint32_t N;
+    int strang;
+    uint64_t W;    // walkers per entry (K3) or total walkers (K4)
+    uint32_t k0, k1; // Philox key = seed
+};
+
+// split_pack.cu
+void launch_validate_csr(uint64_t n, const uint64_t* row_ptr, const uint32_t* col,
+                         const double* val, unsigned long long* err, cudaStream_t s);
+void launch_split_pack(uint64_t n, const uint64_t* row_ptr, const double* weight,
+                       const double* diag, double* d, double* rate, double* cum,
+                       uint8_t* uniform_row, RowRec* rec, unsigned long long* dmax,
+                       unsigned int* any_nonuniform, cudaStream_t s);
+void launch_alias_build(uint64_t n, const uint64_t* row_ptr, const double* weight,
+                        const double* rate, const uint8_t* uniform_row, uint32_t* thr,
+                        uint32_t* alias, double* p, uint32_t* small, uint32_t* large,
+                        cudaStream_t s);
+void launch_pack_v(uint64_t n, const double* v, RowRec* rec, cudaStream_t s);
+void launch_node_factors(uint64_t n, const double* d, double scale, double* f,
+                         cudaStream_t s);
+
+// walk_compat.cu (K2)
+void launch_entry_compat(const DevSplit& m, const double* v, const uint32_t* rows,
+                         uint64_t nrows, double dt, uint64_t n_steps, uint64_t samples,
+                         const double* before, const double* after, uint64_t seed,
+                         double* value, double* se, uint64_t* jumps, cudaStream_t s);
+unsigned scatter_compat_grid();
+void launch_scatter_compat(const DevSplit& m, int start_mode, const double* vcum, double v_sum,
+                           double dt, uint64_t n_steps, uint64_t samples, const double* before,
+                           const double* after, uint64_t seed, double* values, double* part_sum,
+                           double* part_sq, unsigned long long* part_j, cudaStream_t s);
+
+// walk_fast.cu (K3, K4, K6)
+int entry_fast_wpr(uint64_t W);
+void launch_entry_fast(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
+                       const FastParams& p, double* value, double* se, uint64_t* jumps,
+                       cudaStream_t s);
+unsigned scatter_fast_grid();
+void launch_scatter_fast(const DevSplit& m, int start_mode, const double* vcum, double v_sum,
+                         const FastParams& p, double* values, double* part_s1, double* part_s2,
+                         unsigned long long* part_j, cudaStream_t s);
+void launch_gather_ceiling(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
+                           uint32_t chains_per_row, uint32_t chain_len, uint32_t salt,
+                           unsigned long long* sink, cudaStream_t s);
+
+// reduce.cu
+void launch_final_reduce(const double* part_a, const double* part_b,
+                         const unsigned long long* part_c, unsigned nparts, double* out_a,
+                         double* out_b, unsigned long long* out_c, cudaStream_t s);
+void launch_scale(uint64_t n, double* x, double alpha, cudaStream_t s);
+void launch_count_nonfinite(uint64_t n, const double* x, unsigned int* flag, cudaStream_t s);
+
+// expmv.cu (K5)
+void launch_spmv(const DevSplit& m, int mode, double shift, const double* x, double* y,
+                 cudaStream_t s);
+void launch_axpy(uint64_t n, double a, const double* x, double* y, cudaStream_t s);
+void launch_scale_diag(uint64_t n, const double* d, double scale, double* x, cudaStream_t s);
+void launch_norm_inf(uint64_t n, const double* x, double* part, unsigned nparts, cudaStream_t s);
+unsigned norm_parts();
+void launch_dot2(uint64_t n, const double* x, const double* y, double* pa, double* pb,
+                 unsigned long long* pc, unsigned nparts, cudaStream_t s);
+
+}  // namespace expmc_b200

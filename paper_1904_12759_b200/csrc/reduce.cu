@@ -1,0 +1,73 @@
+// Deterministic final reductions over per-block partials (fixed shape:
+// one 256-thread block, thread t sums parts t, t+256, ... in order, then a
+// fixed tree), plus small elementwise helpers.
+#include "kernels.cuh"
+
+namespace expmc_b200 {
+
+namespace {
+
+__global__ void __launch_bounds__(256)
+final_reduce_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                    const unsigned long long* __restrict__ c, unsigned nparts,
+                    double* __restrict__ oa, double* __restrict__ ob,
+                    unsigned long long* __restrict__ oc) {
+    __shared__ double sa[256], sb[256];
+    __shared__ unsigned long long sc[256];
+    double x = 0.0, y = 0.0;
+    unsigned long long z = 0;
+    for (unsigned k = threadIdx.x; k < nparts; k += 256) {
+        x = __dadd_rn(x, a[k]);
+        y = __dadd_rn(y, b[k]);
+        z += c[k];
+    }
+    sa[threadIdx.x] = x;
+    sb[threadIdx.x] = y;
+    sc[threadIdx.x] = z;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) {
+            sa[threadIdx.x] = __dadd_rn(sa[threadIdx.x], sa[threadIdx.x + o]);
+            sb[threadIdx.x] = __dadd_rn(sb[threadIdx.x], sb[threadIdx.x + o]);
+            sc[threadIdx.x] += sc[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *oa = sa[0];
+        *ob = sb[0];
+        *oc = sc[0];
+    }
+}
+
+__global__ void scale_kernel(uint64_t n, double* __restrict__ x, double alpha) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) x[i] = __dmul_rn(x[i], alpha);
+}
+
+__global__ void nonfinite_kernel(uint64_t n, const double* __restrict__ x,
+                                 unsigned int* __restrict__ flag) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const bool bad = i < n && !isfinite(x[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+}  // namespace
+
+void launch_count_nonfinite(uint64_t n, const double* x, unsigned int* flag, cudaStream_t s) {
+    if (n == 0) return;
+    nonfinite_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, x, flag);
+}
+
+void launch_final_reduce(const double* part_a, const double* part_b,
+                         const unsigned long long* part_c, unsigned nparts, double* out_a,
+                         double* out_b, unsigned long long* out_c, cudaStream_t s) {
+    final_reduce_kernel<<<1, 256, 0, s>>>(part_a, part_b, part_c, nparts, out_a, out_b, out_c);
+}
+
+void launch_scale(uint64_t n, double* x, double alpha, cudaStream_t s) {
+    if (n == 0) return;
+    scale_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, x, alpha);
+}
+
+}  // namespace expmc_b200

@@ -1,0 +1,306 @@
+"""Host-side mirror of the reference estimator API, over the C ABI.
+
+Reference interface mirrored (names, argument meaning, errors):
+  PathParams, Splitting, Estimate, VectorEstimate
+      /root/reference/proj/include/expmc/estimator.hpp:11-52
+  entry_estimate / vector_estimate / tc_estimate
+      estimator.hpp:59-72, proj/src/estimator.cpp:169-318
+  split(SparseSymmetric) -> SplitMatrix
+      proj/include/expmc/sparse_matrix.hpp:105, proj/src/sparse_matrix.cpp:101-142
+
+``std::invalid_argument`` maps to ``ValueError`` with the reference's
+message; CUDA / runtime failures raise ``ExpmcError``.  ``workers`` is
+accepted for signature compatibility and ignored (the GPU decides the
+parallelism; results do not depend on it).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import EstimateC, PathParamsC, check, f64p, lib, u8p, u32p, u64p
+
+
+class Splitting(enum.IntEnum):
+    """estimator.hpp:11"""
+    Lie = 0
+    Strang = 1
+
+
+class Rng(enum.IntEnum):
+    """Walker engine: PHILOX = production continuous-clock walker (K3/K4);
+    PCG_COMPAT = path-by-path replay of the reference PCG32 streams (K2)."""
+    PHILOX = 0
+    PCG_COMPAT = 1
+
+
+@dataclass
+class PathParams:
+    """estimator.hpp:16-33 (same defaults)."""
+    beta: float = 1.0
+    n_steps: int = 32
+    samples: int = 1_000_000
+    splitting: Splitting = Splitting.Strang
+    seed: int = 0
+    rng: Rng = Rng.PHILOX
+
+    def dt(self) -> float:
+        return self.beta / float(self.n_steps)
+
+    @staticmethod
+    def with_steps(beta, n_steps, samples, s, seed, rng=Rng.PHILOX) -> "PathParams":
+        p = PathParams(beta, n_steps, samples, s, seed, rng)
+        p.validate()
+        return p
+
+    @staticmethod
+    def with_dt(beta, dt, samples, s, seed, rng=Rng.PHILOX) -> "PathParams":
+        # estimator.cpp:151-159: llround(beta/dt), at least 1
+        if not (beta > 0.0) or not (dt > 0.0):
+            raise ValueError("beta and dt must be positive")
+        q = beta / dt
+        n = max(1, int(math.floor(q + 0.5)) if q >= 0 else int(math.ceil(q - 0.5)))
+        return PathParams.with_steps(beta, n, samples, s, seed, rng)
+
+    def validate(self) -> None:
+        # estimator.cpp:161-167
+        if not (self.beta > 0.0) or not math.isfinite(self.beta):
+            raise ValueError("beta must be positive and finite")
+        if self.n_steps == 0:
+            raise ValueError("n_steps must be >= 1")
+        if self.samples == 0:
+            raise ValueError("samples must be >= 1")
+
+    def _c(self) -> PathParamsC:
+        if self.n_steps < 0 or self.samples < 0 or self.seed < 0:
+            raise ValueError("n_steps, samples and seed must be non-negative")
+        return PathParamsC(float(self.beta), int(self.n_steps), int(self.samples),
+                           int(self.splitting), int(self.rng), int(self.seed) & (2**64 - 1))
+
+
+@dataclass
+class Estimate:
+    """estimator.hpp:37-42"""
+    value: float = 0.0
+    std_error: float = 0.0
+    samples_used: int = 0
+    total_jumps: int = 0
+
+
+@dataclass
+class VectorEstimate:
+    """estimator.hpp:46-52"""
+    values: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    std_error_global: float = 0.0
+    samples_used: int = 0
+    total_jumps: int = 0
+    v_sum: float = 0.0
+
+
+@dataclass
+class EntriesEstimate:
+    """Batched entry_estimate over many rows ("full vector with W walkers
+    per entry"): per-row value, standard error and jump count."""
+    rows: np.ndarray
+    values: np.ndarray
+    std_errors: np.ndarray
+    jumps: np.ndarray
+    samples_per_entry: int
+
+    @property
+    def total_jumps(self) -> int:
+        return int(self.jumps.sum())
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class SplitMatrix:
+    """Device-resident SplitMatrix (sparse_matrix.hpp:66-91) on one GPU.
+
+    Built by :func:`split` from the mirrored adjacency of a symmetric matrix;
+    immutable afterwards.  ``export()`` copies the reference's fields back to
+    host memory (for parity checks)."""
+
+    def __init__(self, handle, csr_n):
+        self._h = handle
+        n, nnz, dbar, dmax = C.c_uint64(), C.c_uint64(), C.c_double(), C.c_uint64()
+        anu, dev = C.c_int32(), C.c_int32()
+        check(lib().expmc_cuda_matrix_info(handle, C.byref(n), C.byref(nnz), C.byref(dbar),
+                                           C.byref(dmax), C.byref(anu), C.byref(dev)))
+        self.n, self.nnz = n.value, nnz.value
+        self.dbar, self.dmax = dbar.value, dmax.value
+        self.any_nonuniform = bool(anu.value)
+        self.device = dev.value
+
+    @classmethod
+    def from_csr(cls, n, row_ptr, col, val, diag=None, device=0) -> "SplitMatrix":
+        row_ptr = np.ascontiguousarray(row_ptr, dtype=np.uint64)
+        col = np.ascontiguousarray(col, dtype=np.uint32)
+        val = _f64(val)
+        diag = None if diag is None else _f64(diag)
+        if len(row_ptr) != n + 1:
+            raise ValueError("row_ptr must have n + 1 entries")
+        h = C.c_void_p()
+        check(lib().expmc_cuda_create_from_csr(
+            n, row_ptr.ctypes.data_as(u64p), col.ctypes.data_as(u32p),
+            val.ctypes.data_as(f64p), None if diag is None else diag.ctypes.data_as(f64p),
+            int(device), C.byref(h)))
+        return cls(h, n)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            lib().expmc_cuda_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def export(self) -> dict:
+        n, nnz = self.n, self.nnz
+        s = dict(diag=np.zeros(n), d=np.zeros(n), rate=np.zeros(n),
+                 row_offset=np.zeros(n + 1, np.uint64), neighbor=np.zeros(nnz, np.uint32),
+                 weight=np.zeros(nnz), cum=np.zeros(nnz), uniform_row=np.zeros(n, np.uint8))
+        check(lib().expmc_cuda_split_export(
+            self._h, s["diag"].ctypes.data_as(f64p), s["d"].ctypes.data_as(f64p),
+            s["rate"].ctypes.data_as(f64p), s["row_offset"].ctypes.data_as(u64p),
+            s["neighbor"].ctypes.data_as(u32p), s["weight"].ctypes.data_as(f64p),
+            s["cum"].ctypes.data_as(f64p), s["uniform_row"].ctypes.data_as(u8p)))
+        s["dbar"], s["dmax"] = self.dbar, self.dmax
+        return s
+
+    def alias_tables(self):
+        thr = np.zeros(self.nnz, np.uint32)
+        al = np.zeros(self.nnz, np.uint32)
+        check(lib().expmc_cuda_alias_export(self._h, thr.ctypes.data_as(u32p),
+                                            al.ctypes.data_as(u32p)))
+        return thr, al
+
+    REC = np.dtype([("off", "<u4"), ("degf", "<u4"), ("inv_rate", "<f4"), ("spare", "<u4"),
+                    ("d", "<f8"), ("v", "<f8")])
+
+    def records(self) -> np.ndarray:
+        out = np.zeros(self.n, self.REC)
+        check(lib().expmc_cuda_records_export(self._h, out.ctypes.data))
+        return out
+
+
+def split(csr, device=0) -> SplitMatrix:
+    """split(SparseSymmetric) (sparse_matrix.cpp:101-142), on the GPU.
+    ``csr`` has ``n, row_ptr, col, val, diag`` (see :class:`inputs.Csr`)."""
+    return SplitMatrix.from_csr(csr.n, csr.row_ptr, csr.col, csr.val, csr.diag, device)
+
+
+def entry_slots(walkers: int) -> int:
+    """Lane slots per entry of the Philox walker (result contract)."""
+    return int(lib().expmc_cuda_entry_slots(int(walkers)))
+
+
+def entry_estimate(m: SplitMatrix, v, i: int, p: PathParams, workers: int = 1) -> Estimate:
+    """estimator.cpp:169-206 — entry i of the splitting approximation."""
+    v = _f64(v)
+    if i < 0 or i >= 2**32:
+        raise ValueError("entry index out of range")
+    out = EstimateC()
+    pc = p._c()
+    check(lib().expmc_cuda_entry_estimate(m.handle, v.ctypes.data_as(f64p), len(v), int(i),
+                                          C.byref(pc), C.byref(out)))
+    return Estimate(out.value, out.std_error, out.samples_used, out.total_jumps)
+
+
+def entries_estimate(m: SplitMatrix, v, rows, p: PathParams) -> EntriesEstimate:
+    """Batched entry_estimate: rows=None means every row (full vector)."""
+    v = _f64(v)
+    pc = p._c()
+    if rows is None:
+        nrows = m.n
+        rp = None
+        rows_arr = np.arange(m.n, dtype=np.uint32)
+    else:
+        rows_arr = np.asarray(rows)
+        if rows_arr.size and (rows_arr.min() < 0 or rows_arr.max() >= 2**32):
+            raise ValueError("entry index out of range")
+        rows_arr = np.ascontiguousarray(rows_arr, dtype=np.uint32)
+        nrows = len(rows_arr)
+        rp = rows_arr.ctypes.data_as(u32p)
+    val, se, jm = np.zeros(nrows), np.zeros(nrows), np.zeros(nrows, np.uint64)
+    check(lib().expmc_cuda_entries(m.handle, v.ctypes.data_as(f64p), len(v), rp, nrows,
+                                   C.byref(pc), val.ctypes.data_as(f64p),
+                                   se.ctypes.data_as(f64p), jm.ctypes.data_as(u64p)))
+    return EntriesEstimate(rows_arr, val, se, jm, p.samples)
+
+
+def vector_estimate(m: SplitMatrix, v, p: PathParams, workers: int = 1) -> VectorEstimate:
+    """estimator.cpp:208-278 — Theorem 2 full-vector estimator (v >= 0)."""
+    v = _f64(v)
+    pc = p._c()
+    vals = np.zeros(m.n)
+    se, jm, vs = C.c_double(), C.c_uint64(), C.c_double()
+    check(lib().expmc_cuda_vector_estimate(m.handle, v.ctypes.data_as(f64p), len(v),
+                                           C.byref(pc), vals.ctypes.data_as(f64p),
+                                           C.byref(se), C.byref(jm), C.byref(vs)))
+    return VectorEstimate(vals, se.value, p.samples, jm.value, vs.value)
+
+
+def tc_estimate(m: SplitMatrix, p: PathParams, workers: int = 1) -> Estimate:
+    """estimator.cpp:280-318 — total communicability (1, e^{βA} 1)."""
+    pc = p._c()
+    out = EstimateC()
+    check(lib().expmc_cuda_tc_estimate(m.handle, C.byref(pc), C.byref(out)))
+    return Estimate(out.value, out.std_error, out.samples_used, out.total_jumps)
+
+
+def expmv(m: SplitMatrix, v, t: float, tol: float = 1e-15) -> np.ndarray:
+    """Deterministic fp64 exp(tA)v on the GPU (K5; accuracy reference)."""
+    v = _f64(v)
+    out = np.zeros(m.n)
+    check(lib().expmc_cuda_expmv(m.handle, v.ctypes.data_as(f64p), len(v), float(t),
+                                 float(tol), out.ctypes.data_as(f64p)))
+    return out
+
+
+def splitting_product(m: SplitMatrix, v, p: PathParams, tol: float = 1e-15) -> np.ndarray:
+    """Deterministic splitting product the estimators sample (K5)."""
+    v = _f64(v)
+    pc = p._c()
+    out = np.zeros(m.n)
+    check(lib().expmc_cuda_splitting_product(m.handle, v.ctypes.data_as(f64p), len(v),
+                                             C.byref(pc), float(tol),
+                                             out.ctypes.data_as(f64p)))
+    return out
+
+
+# ------------------------------------------------- device-resident entry API
+def set_v_device(m: SplitMatrix, v_ptr: int, n: int, stream: int = 0) -> None:
+    check(lib().expmc_cuda_set_v_device(m.handle, v_ptr, n, stream or None))
+
+
+def entries_device(m: SplitMatrix, rows_ptr: int, nrows: int, p: PathParams, value_ptr: int,
+                   se_ptr: int, jumps_ptr: int, stream: int = 0) -> None:
+    """Async Philox entry walker on device buffers (raw device pointers)."""
+    pc = p._c()
+    check(lib().expmc_cuda_entries_device(m.handle, rows_ptr, nrows, C.byref(pc), value_ptr,
+                                          se_ptr, jumps_ptr, stream or None))
+
+
+def gather_ceiling_device(m: SplitMatrix, rows_ptr: int, nrows: int, chains_per_row: int,
+                          chain_len: int, stream: int = 0) -> None:
+    check(lib().expmc_cuda_gather_ceiling_device(m.handle, rows_ptr, nrows,
+                                                 int(chains_per_row), int(chain_len),
+                                                 stream or None))
+
+
+def launch_count() -> int:
+    return int(lib().expmc_cuda_launch_count())

@@ -1,0 +1,342 @@
+"""GPU parity tests (B200): the CUDA path through the C ABI against the
+oracle (oracle/liboracle.so) and the compiled reference (oracle/_ref).
+
+Tolerances (written here, per the contract):
+  * split_pack (K1): bit-exact (rate, cum, d, uniform_row, dbar, dmax, alias).
+  * PCG-compat walker (K2) vs reference entry_estimate(workers=1): value and
+    std_error to 1e-12 relative (summation order only), total_jumps exact.
+  * Philox walker (K3) vs its CPU model: 1e-12 relative, jumps exact.
+  * Philox walker vs the reference: statistical, |z| <= 4 per entry with a
+    binomial allowance plus z-histogram mean/variance checks.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _graphs(pb):
+    out = {
+        "p3": pb.csr_from_dense(np.array([[0.0, 1, 0], [1, 0.5, 3], [0, 3, 0]])),
+        "fd2d_16": pb.gen_fd(2, 16, 1.0),
+        "ba_2000": pb.gen_ba(2000, 5, 1),
+        "ws_3000": pb.gen_ws(3000, 5, 0.1, 1),
+        "fd3d_10": pb.gen_fd(3, 10, 121.0),
+    }
+    rng = np.random.default_rng(5)
+    a = np.zeros((40, 40))
+    for _ in range(120):
+        i, j = rng.integers(0, 40, 2)
+        if i != j:
+            a[i, j] = a[j, i] = float(rng.integers(1, 5)) * 0.5
+    np.fill_diagonal(a, rng.normal(size=40))
+    out["weighted_40"] = pb.csr_from_dense(a)
+    return out
+
+
+@pytest.fixture(scope="module")
+def graphs(pb):
+    return _graphs(pb)
+
+
+def test_split_pack_bit_exact(pb, ref, orc, graphs):
+    for name, csr in graphs.items():
+        m = pb.split(csr)
+        dev = m.export()
+        rs = ref.matrix_from_csr(csr).split()
+        for k in ("diag", "d", "rate", "cum", "uniform_row", "row_offset", "neighbor", "weight"):
+            assert np.array_equal(dev[k], rs[k]), (name, k)
+        assert m.dbar == rs["dbar"] and m.dmax == rs["dmax"], name
+        thr, al = m.alias_tables()
+        othr, oal = orc.alias_build(rs)
+        assert np.array_equal(thr, othr) and np.array_equal(al, oal), name
+        rec = m.records()
+        assert np.array_equal(rec["d"], rs["d"])
+        assert np.array_equal(rec["inv_rate"], (1.0 / rs["rate"]).astype(np.float32))
+
+
+def test_alias_tables_reproduce_weights(pb, graphs):
+    csr = graphs["weighted_40"]
+    m = pb.split(csr)
+    thr, al = m.alias_tables()
+    s = m.export()
+    for i in range(csr.n):
+        lo, hi = int(s["row_offset"][i]), int(s["row_offset"][i + 1])
+        deg = hi - lo
+        if deg == 0 or s["uniform_row"][i]:
+            continue
+        prob = np.zeros(deg)
+        for k in range(deg):
+            keep = thr[lo + k] / 2.0 ** 32
+            prob[k] += keep / deg
+            prob[al[lo + k]] += (1 - keep) / deg
+        np.testing.assert_allclose(prob, s["weight"][lo:hi] / s["rate"][i], atol=1e-9)
+
+
+@pytest.mark.parametrize("splitting", [0, 1])
+def test_pcg_compat_entries_match_reference(pb, ref, graphs, splitting):
+    for name in ("p3", "fd2d_16", "ba_2000", "weighted_40"):
+        csr = graphs[name]
+        rm = ref.matrix_from_csr(csr)
+        m = pb.split(csr)
+        v = pb.gen_vector(1, csr.n, 7)
+        rows = np.unique(np.linspace(0, csr.n - 1, min(csr.n, 24)).astype(np.uint32))
+        W = 3000 if name != "p3" else 100_000
+        beta = 1.0 if name != "ba_2000" else 0.05
+        p = pb.PathParams(beta, 8, W, pb.Splitting(splitting), 2024, pb.Rng.PCG_COMPAT)
+        got = pb.entries_estimate(m, v, rows, p)
+        rv, rse, rj = rm.entries(v, rows, beta, 8, W, splitting, 2024, workers=1)
+        np.testing.assert_allclose(got.values, rv, rtol=1e-12, atol=1e-300, err_msg=name)
+        np.testing.assert_allclose(got.std_errors, rse, rtol=1e-9, atol=1e-300, err_msg=name)
+        assert np.array_equal(got.jumps, rj), name
+
+
+def test_p3_golden(pb):
+    """SURVEY §8a fixture: reference entry_estimate values, reproduced by K2."""
+    csr = pb.csr_from_dense(np.array([[0.0, 1, 0], [1, 0.5, 3], [0, 3, 0]]))
+    m = pb.split(csr)
+    v = np.array([1.0, 2.0, -0.5])
+    e = pb.entry_estimate(m, v, 1, pb.PathParams(1.0, 8, 100_000, pb.Splitting.Strang, 2024,
+                                                 pb.Rng.PCG_COMPAT))
+    assert abs(e.value - 31.248671410962384) <= 1e-12 * 31.25
+    assert e.total_jumps == 308153
+    e = pb.entry_estimate(m, v, 1, pb.PathParams(1.0, 8, 100_000, pb.Splitting.Lie, 2024,
+                                                 pb.Rng.PCG_COMPAT))
+    assert abs(e.value - 30.938284991716518) <= 1e-12 * 30.94
+    assert e.total_jumps == 308153
+
+
+@pytest.mark.parametrize("W", [1000, 5000, 10000])
+@pytest.mark.parametrize("splitting", [0, 1])
+def test_philox_walker_matches_cpu_model(pb, orc, graphs, W, splitting):
+    for name in ("p3", "fd2d_16", "ba_2000", "weighted_40", "fd3d_10"):
+        csr = graphs[name]
+        m = pb.split(csr)
+        s = orc.split(csr)
+        v = pb.gen_vector(1, csr.n, 9)
+        rows = np.unique(np.linspace(0, csr.n - 1, min(csr.n, 12)).astype(np.uint32))
+        beta = {"ba_2000": 0.05, "fd3d_10": 0.02}.get(name, 1.0)
+        p = pb.PathParams(beta, 32, W, pb.Splitting(splitting), 77, pb.Rng.PHILOX)
+        got = pb.entries_estimate(m, v, rows, p)
+        mv, ms, mj = orc.fast_entries(s, v, rows, beta, 32, W, splitting, 77, pb.entry_slots(W))
+        np.testing.assert_allclose(got.values, mv, rtol=1e-12, atol=1e-300, err_msg=name)
+        np.testing.assert_allclose(got.std_errors, ms, rtol=1e-9, atol=1e-300, err_msg=name)
+        assert np.array_equal(got.jumps, mj), name
+
+
+def _zcheck(z, K):
+    z = np.asarray(z)
+    bad = int(np.sum(np.abs(z) > 4.0))
+    # binomial allowance for K entries at P(|z|>4) = 6.3e-5 (+ heavy tails)
+    assert bad <= 2 + int(6.3e-5 * K * 10), (bad, K)
+    if K >= 200:
+        assert abs(z.mean()) < 0.2 and 0.6 < z.var() < 1.5, (z.mean(), z.var())
+
+
+@pytest.mark.parametrize("splitting", [0, 1])
+def test_philox_walker_statistically_matches_reference(pb, ref, graphs, splitting):
+    zs = []
+    for name in ("fd2d_16", "ba_2000", "ws_3000", "weighted_40"):
+        csr = graphs[name]
+        rm = ref.matrix_from_csr(csr)
+        m = pb.split(csr)
+        v = pb.gen_vector(0, csr.n, 4) + 0.5
+        rows = np.unique(np.linspace(0, csr.n - 1, min(csr.n, 64)).astype(np.uint32))
+        beta = {"ba_2000": 0.05, "ws_3000": 0.3}.get(name, 1.0)
+        W = 20000
+        got = pb.entries_estimate(m, v, rows,
+                                  pb.PathParams(beta, 32, W, pb.Splitting(splitting), 11))
+        rv, rse, _ = rm.entries(v, rows, beta, 32, W, splitting, 12, workers=1, threads=8)
+        zs.append((got.values - rv) / np.sqrt(got.std_errors ** 2 + rse ** 2 + 1e-300))
+    _zcheck(np.concatenate(zs), sum(len(z) for z in zs))
+
+
+def test_kat_empty_graph_and_single_edge(pb):
+    # empty graph: value = v_i exactly, SE 0
+    csr = pb.csr_from_dense(np.diag([0.0, 0.0, 0.0]))
+    m = pb.split(csr)
+    for rng in (pb.Rng.PHILOX, pb.Rng.PCG_COMPAT):
+        e = pb.entry_estimate(m, [1.0, 2.0, 3.0], 2, pb.PathParams(1.0, 32, 1000, rng=rng))
+        assert e.value == 3.0 and e.std_error == 0.0 and e.total_jumps == 0
+        t = pb.tc_estimate(m, pb.PathParams(1.0, 32, 1000, rng=rng))
+        assert t.value == 3.0 and t.std_error == 0.0
+    # single edge: entry (0,0) of e^A with v=(1,0) = cosh 1; TC = 2e
+    csr = pb.csr_from_dense(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    m = pb.split(csr)
+    for rng in (pb.Rng.PHILOX, pb.Rng.PCG_COMPAT):
+        e = pb.entry_estimate(m, [1.0, 0.0], 0, pb.PathParams(1.0, 32, 1_000_000, seed=7, rng=rng))
+        assert abs(e.value - math.cosh(1.0)) < 4 * e.std_error + 1e-12
+        t = pb.tc_estimate(m, pb.PathParams(1.0, 32, 1_000_000, seed=7, rng=rng))
+        assert abs(t.value - 2 * math.e) < 1e-9  # regular graph: deterministic weight
+        ve = pb.vector_estimate(m, [1.0, 1.0], pb.PathParams(1.0, 32, 1_000_000, seed=7, rng=rng))
+        assert np.all(np.abs(ve.values - math.e) < 0.01)
+        assert abs(ve.values.sum() - 2 * math.e) < 1e-9
+
+
+@pytest.mark.parametrize("splitting", [0, 1])
+def test_pcg_compat_vector_and_tc_match_reference(pb, ref, graphs, splitting):
+    for name in ("fd2d_16", "weighted_40"):
+        csr = graphs[name]
+        rm = ref.matrix_from_csr(csr)
+        m = pb.split(csr)
+        v = pb.gen_vector(0, csr.n, 3)
+        M = 200_000
+        p = pb.PathParams(0.7, 16, M, pb.Splitting(splitting), 5, pb.Rng.PCG_COMPAT)
+        got = pb.vector_estimate(m, v, p)
+        rv, rse, rj, rvs = rm.vector_estimate(v, 0.7, 16, M, splitting, 5, workers=1)
+        np.testing.assert_allclose(got.values, rv, rtol=1e-11, atol=1e-14)
+        assert abs(got.std_error_global - rse) <= 1e-9 * rse
+        assert got.total_jumps == rj and got.v_sum == rvs
+        t = pb.tc_estimate(m, p)
+        tv, tse, tj = rm.tc_estimate(0.7, 16, M, splitting, 5, workers=1)
+        assert abs(t.value - tv) <= 1e-12 * abs(tv)
+        assert abs(t.std_error - tse) <= 1e-9 * tse
+        assert t.total_jumps == tj
+
+
+@pytest.mark.parametrize("splitting", [0, 1])
+def test_philox_vector_and_tc_statistical(pb, ref, graphs, splitting):
+    csr = graphs["fd2d_16"]
+    rm = ref.matrix_from_csr(csr)
+    m = pb.split(csr)
+    v = pb.gen_vector(0, csr.n, 3)
+    M = 2_000_000
+    p = pb.PathParams(1.0, 32, M, pb.Splitting(splitting), 5)
+    got = pb.vector_estimate(m, v, p)
+    rv, rse, rj, rvs = rm.vector_estimate(v, 1.0, 32, M, splitting, 6, workers=8)
+    # global scalar functional: sum(values) = mean of V w
+    z = (got.values.sum() - rv.sum()) / math.sqrt(got.std_error_global ** 2 + rse ** 2)
+    assert abs(z) < 4.0
+    rel = np.abs(got.values - rv).sum() / np.abs(rv).sum()
+    assert rel < 0.02
+    t = pb.tc_estimate(m, p)
+    tv, tse, _ = rm.tc_estimate(1.0, 32, M, splitting, 6, workers=8)
+    assert abs(t.value - tv) < 4.0 * math.sqrt(t.std_error ** 2 + tse ** 2)
+
+
+def test_expmv_and_splitting_product(pb, graphs):
+    scipy = pytest.importorskip("scipy.sparse.linalg")
+    import scipy.sparse as sp
+
+    for name in ("fd2d_16", "weighted_40", "ba_2000"):
+        csr = graphs[name]
+        m = pb.split(csr)
+        n = csr.n
+        A = sp.csr_matrix((csr.val, csr.col.astype(np.int64), csr.row_ptr.astype(np.int64)),
+                          shape=(n, n)) + sp.diags(csr.diag)
+        v = pb.gen_vector(0, n, 1)
+        t = 0.5 if name != "ba_2000" else 0.05
+        want = scipy.expm_multiply(t * A.tocsc(), v)
+        got = pb.expmv(m, v, t)
+        np.testing.assert_allclose(got, want, rtol=1e-10, atol=1e-12 * np.abs(want).max())
+        if n <= 300:
+            import scipy.linalg as sl
+
+            Ad = A.toarray()
+            L = np.diag(np.asarray(np.abs(A - sp.diags(csr.diag)).sum(axis=1)).ravel()) - \
+                (Ad - np.diag(csr.diag))
+            D = np.diag(csr.diag + np.diag(L))
+            for splitting in (0, 1):
+                N = 8
+                dt = t / N
+                if splitting == 1:
+                    P = sl.expm(D * dt / 2) @ sl.expm(-L * dt) @ sl.expm(D * dt / 2)
+                else:
+                    P = sl.expm(-L * dt) @ sl.expm(D * dt)
+                want_s = np.linalg.matrix_power(P, N) @ v
+                got_s = pb.splitting_product(m, v, pb.PathParams(t, N, 1, pb.Splitting(splitting)))
+                np.testing.assert_allclose(got_s, want_s, rtol=1e-10, atol=1e-13)
+
+
+def test_lambda_max_matches_reference(pb, ref, graphs):
+    for name in ("ba_2000", "fd2d_16", "weighted_40"):
+        csr = graphs[name]
+        lam = pb.lambda_max(pb.split(csr), 100)
+        want = ref.matrix_from_csr(csr).lambda_max(100)
+        assert abs(lam - want) <= 1e-10 * abs(want), (name, lam, want)
+
+
+def test_error_messages_match_reference(pb, ref, graphs):
+    csr = graphs["fd2d_16"]
+    m = pb.split(csr)
+    v = np.ones(csr.n)
+    rm = ref.matrix_from_csr(csr)
+    cases = [
+        (lambda: pb.entry_estimate(m, v, 0, pb.PathParams(beta=-1.0)), "beta must be positive and finite"),
+        (lambda: pb.entry_estimate(m, v, 0, pb.PathParams(n_steps=0)), "n_steps must be >= 1"),
+        (lambda: pb.entry_estimate(m, v, 0, pb.PathParams(samples=0)), "samples must be >= 1"),
+        (lambda: pb.entry_estimate(m, v[:-1], 0, pb.PathParams(samples=10)), "vector length does not match matrix"),
+        (lambda: pb.entry_estimate(m, np.r_[v[:-1], np.nan], 0, pb.PathParams(samples=10)), "non-finite entry in v"),
+        (lambda: pb.entry_estimate(m, v, csr.n, pb.PathParams(samples=10)), "entry index out of range"),
+        (lambda: pb.vector_estimate(m, -v, pb.PathParams(samples=10)), "vector_estimate requires v >= 0 entrywise"),
+        (lambda: pb.vector_estimate(m, 0 * v, pb.PathParams(samples=10)), "vector_estimate requires sum(v) > 0"),
+    ]
+    for fn, msg in cases:
+        with pytest.raises(ValueError) as ei:
+            fn()
+        assert str(ei.value) == msg
+    # the reference raises the same text
+    import oracle
+
+    with pytest.raises(oracle.RefError, match="entry index out of range"):
+        rm.entry_estimate(v, csr.n, 1.0, 32, 10)
+    empty = pb.split(pb.Csr(0, np.zeros(1, np.uint64), np.zeros(0, np.uint32), np.zeros(0),
+                            np.zeros(0)))
+    with pytest.raises(ValueError, match="empty matrix"):
+        pb.tc_estimate(empty, pb.PathParams(samples=10))
+
+
+def test_csr_validation_messages(pb):
+    bad = pb.csr_from_dense(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    asym = pb.Csr(2, bad.row_ptr, bad.col, np.array([1.0, 2.0]), bad.diag)
+    with pytest.raises(ValueError, match=r"not symmetric at \(0, 1\)"):
+        pb.split(asym)
+    neg = pb.Csr(2, bad.row_ptr, bad.col, np.array([-1.0, -1.0]), bad.diag)
+    with pytest.raises(ValueError, match=r"negative off-diagonal weight at \(0, 1\)"):
+        pb.split(neg)
+    zero = pb.Csr(2, bad.row_ptr, bad.col, np.array([0.0, 0.0]), bad.diag)
+    with pytest.raises(ValueError, match=r"explicit zero entry at \(0, 1\)"):
+        pb.split(zero)
+    oob = pb.Csr(2, bad.row_ptr, np.array([5, 0], np.uint32), bad.val, bad.diag)
+    with pytest.raises(ValueError, match="out of range for n = 2"):
+        pb.split(oob)
+
+
+def test_device_api_matches_host_api(pb, graphs):
+    torch = pytest.importorskip("torch")
+    csr = graphs["ba_2000"]
+    m = pb.split(csr)
+    v = pb.gen_vector(1, csr.n, 2)
+    p = pb.PathParams(0.05, 32, 1000, pb.Splitting.Strang, 3)
+    host = pb.entries_estimate(m, v, None, p)
+    vd = torch.from_numpy(v).cuda()
+    rows = torch.arange(csr.n, dtype=torch.int32, device="cuda")
+    val = torch.empty(csr.n, dtype=torch.float64, device="cuda")
+    se = torch.empty_like(val)
+    jm = torch.empty(csr.n, dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    pb.set_v_device(m, vd.data_ptr(), csr.n, stream)
+    pb.entries_device(m, rows.data_ptr(), csr.n, p, val.data_ptr(), se.data_ptr(),
+                      jm.data_ptr(), stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(val.cpu().numpy(), host.values)
+    assert np.array_equal(se.cpu().numpy(), host.std_errors)
+    assert np.array_equal(jm.cpu().numpy().astype(np.uint64), host.jumps)
+
+
+def test_results_invariant_to_row_sharding(pb, graphs):
+    """Keyed RNG + fixed reduction: any row partition gives identical bits."""
+    csr = graphs["ws_3000"]
+    m = pb.split(csr)
+    v = np.ones(csr.n)
+    p = pb.PathParams(0.05, 32, 2000, pb.Splitting.Strang, 3)
+    full = pb.entries_estimate(m, v, None, p)
+    from paper_1904_12759_b200.shard import plan_shards
+
+    rows = np.arange(csr.n, dtype=np.uint32)
+    for world in (2, 3, 8):
+        parts = [pb.entries_estimate(m, v, rows[lo:hi], p) for lo, hi in plan_shards(csr.n, world)]
+        assert np.array_equal(np.concatenate([q.values for q in parts]), full.values)
+        assert np.array_equal(np.concatenate([q.jumps for q in parts]), full.jumps)
