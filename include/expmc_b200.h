@@ -15,7 +15,7 @@
  *     should be used by one host thread at a time.
  *   - Host-buffer calls are synchronous and blocking, like the reference.
  *   - *_device calls take device pointers on the handle's device and a
- *     cudaStream_t passed as void* (NULL = the handle's own stream); they
+ *     cudaStream_t passed as void* (NULL = the legacy default stream); they
  *     are asynchronous on that stream.
  */
 #ifndef EXPMC_B200_H_

@@ -1,6 +1,6 @@
 /*
  * TEST INFRASTRUCTURE ONLY — a CPU model of the B200 production walker
- * (K3 entry_fast_kernel, paper_1904_12759_b200/csrc/walk_fast.cu), written
+ * (K3 entry_walk_kernel, paper_1904_12759_b200/csrc/walk_entry.cu), written
  * independently from the kernel's contract so the GPU can be pinned walker
  * for walker, not only statistically.
  *
@@ -61,14 +61,17 @@ float fm_neg_ln_u(uint32_t w) {
         m = m * 0.5f;
         e += 1;
     }
-    const float s = (m - 1.0f) / (m + 1.0f);
-    const float z = s * s;
-    float p = fmaf(z, 0.11111111f, 0.14285715f);
-    p = fmaf(z, p, 0.2f);
-    p = fmaf(z, p, 0.33333334f);
-    p = fmaf(z, p, 1.0f);
-    const float lnm = (2.0f * s) * p;
-    const float ln_u = fmaf((float)e, 0.693147182f, lnm);
+    const float f = m - 1.0f;
+    float q = 0.08743945509195328f;
+    q = fmaf(q, f, -0.14377330243587494f);
+    q = fmaf(q, f, 0.14949095249176025f);
+    q = fmaf(q, f, -0.16560696065425873f);
+    q = fmaf(q, f, 0.19956977665424347f);
+    q = fmaf(q, f, -0.2500215470790863f);
+    q = fmaf(q, f, 0.3333418369293213f);
+    q = fmaf(q, f, -0.49999988079071045f);
+    q = fmaf(q, f, 1.0f);
+    const float ln_u = fmaf((float)e, 0.693147182f, f * q);
     return -ln_u;
 }
 
@@ -92,8 +95,55 @@ void fm_build_records(uint64_t n, const uint64_t* row_ptr, const double* rate,
     }
 }
 
-/* One row: per-slot sequential sums over walkers l = slot, slot+T, ...;
- * xor-butterfly within each warp; warps summed in index order. */
+/* Deviation f - f0 of walker l of row i (0 for walkers that never jump).
+ * Word schedule of the kernel: first holding time from the decision word
+ * (counter 0xffffffff, 128*(l/128) + l%32, i, tag; word (l%128)/32); jump j
+ * from counter (j, l, i, tag): y,w = 64-bit pick, z = alias coin, x = next
+ * holding time. */
+static double fm_walker(const fm_rec* rec, const uint32_t* nbr, const uint32_t* thr,
+                        const uint32_t* alias, uint32_t i, uint64_t l, uint64_t T0,
+                        double f0, double corr_i, double dt, double inv_dt, double n_grid,
+                        uint64_t N, int strang, uint32_t k0, uint32_t k1,
+                        uint64_t* jumps) {
+    const uint32_t base = (uint32_t)((l / 128) * 128);
+    const uint32_t dctr[4] = {0xffffffffu, base + (uint32_t)(l % 32), i, FM_TAG_ENTRY};
+    uint32_t dw[4];
+    fm_philox(dctr, k0, k1, dw);
+    const uint32_t ew0 = dw[(l % 128) / 32];
+    if ((uint64_t)ew0 < T0) return 0.0; /* never jumps */
+    fm_rec cur = rec[i];
+    uint32_t ew = ew0, g = 0, jc = 0;
+    double t = 0.0, S = 0.0;
+    for (;;) {
+        const float h = fm_neg_ln_u(ew) * cur.inv_rate;
+        const double tn = t + (double)h * inv_dt;
+        if (tn >= n_grid) {
+            S = fma(cur.d, (double)(N + 1 - g), S);
+            const double corr = strang ? corr_i + 0.5 * cur.d : corr_i;
+            const double x = dt * (S - corr);
+            *jumps += jc;
+            return exp(x) * cur.v - f0;
+        }
+        const uint32_t kk = (uint32_t)ceil(tn);
+        S = fma(cur.d, (double)(kk - g), S);
+        g = kk;
+        t = tn;
+        const uint32_t ctr[4] = {jc, (uint32_t)l, i, FM_TAG_ENTRY};
+        uint32_t w[4];
+        fm_philox(ctr, k0, k1, w);
+        uint32_t k = fm_pick(w[1], w[3], cur.degf & FM_DEGMASK);
+        if (cur.degf & FM_NONUNIFORM) {
+            if (w[2] >= thr[cur.off + k]) k = alias[cur.off + k];
+        }
+        cur = rec[nbr[cur.off + k]];
+        ew = w[0];
+        ++jc;
+    }
+}
+
+/* Accumulation contract of the kernel: lane s of warp w (of WPR = T/32
+ * warps) sums walkers l = s (mod 32) with floor(l/128) = w (mod WPR) in
+ * increasing l; xor butterfly over lanes; warps in index order. */
 void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
                 const uint32_t* thr, const uint32_t* alias, const uint32_t* rows,
                 uint64_t nrows, double beta, uint64_t N, uint64_t W, int strang,
@@ -103,11 +153,8 @@ void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
     const double inv_dt = 1.0 / dt;
     const double n_grid = (double)N;
     const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
-    double* a1 = (double*)malloc(sizeof(double) * T);
-    double* a2 = (double*)malloc(sizeof(double) * T);
-    uint64_t* aj = (uint64_t*)malloc(sizeof(uint64_t) * T);
-    double b1[32], b2[32];
-    uint64_t bj[32];
+    const uint32_t wpr = T / 32;
+    const uint64_t nch = (W + 127) / 128;
     for (uint64_t r = 0; r < nrows; ++r) {
         const uint32_t i = rows[r];
         const fm_rec ri = rec[i];
@@ -115,53 +162,26 @@ void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
         const uint64_t T0 = (uint64_t)(p0 * 4294967296.0);
         const double f0 = exp(beta * ri.d) * ri.v;
         const double corr_i = strang ? 0.5 * ri.d : ri.d;
-        for (uint32_t slot = 0; slot < T; ++slot) {
-            double s1 = 0.0, s2 = 0.0;
-            uint64_t jt = 0;
-            for (uint64_t l = slot; l < W; l += T) {
-                fm_rec cur = ri;
-                double t = 0.0, S = 0.0;
-                uint32_t g = 0, step = 0, jc = 0;
-                for (;;) {
-                    const uint32_t ctr[4] = {step, (uint32_t)l, i, FM_TAG_ENTRY};
-                    uint32_t w[4];
-                    fm_philox(ctr, k0, k1, w);
-                    if (step == 0 && (uint64_t)w[0] < T0) break; /* never jumps */
-                    const float h = fm_neg_ln_u(w[0]) * cur.inv_rate;
-                    const double tn = t + (double)h * inv_dt;
-                    if (tn >= n_grid) {
-                        S = fma(cur.d, (double)(N + 1 - g), S);
-                        const double corr = strang ? corr_i + 0.5 * cur.d : corr_i;
-                        const double f = exp(dt * (S - corr)) * cur.v;
-                        const double dev = f - f0;
-                        s1 = s1 + dev;
-                        s2 = fma(dev, dev, s2);
-                        jt += jc;
-                        break;
-                    }
-                    const uint32_t kk = (uint32_t)ceil(tn);
-                    S = fma(cur.d, (double)(kk - g), S);
-                    g = kk;
-                    t = tn;
-                    const uint32_t deg = cur.degf & FM_DEGMASK;
-                    uint32_t k = fm_pick(w[1], w[3], deg);
-                    if (cur.degf & FM_NONUNIFORM) {
-                        if (w[2] >= thr[cur.off + k]) k = alias[cur.off + k];
-                    }
-                    cur = rec[nbr[cur.off + k]];
-                    ++jc;
-                    ++step;
-                }
-            }
-            a1[slot] = s1;
-            a2[slot] = s2;
-            aj[slot] = jt;
-        }
-        /* butterfly per warp */
         double w1 = 0.0, w2 = 0.0;
         uint64_t wj = 0;
-        for (uint32_t wbase = 0; wbase < T; wbase += 32) {
-            for (int q = 0; q < 32; ++q) { b1[q] = a1[wbase + q]; b2[q] = a2[wbase + q]; bj[q] = aj[wbase + q]; }
+        for (uint32_t wi = 0; wi < wpr; ++wi) {
+            double b1[32], b2[32];
+            uint64_t bj[32];
+            for (int s = 0; s < 32; ++s) { b1[s] = 0.0; b2[s] = 0.0; bj[s] = 0; }
+            for (uint64_t c = wi; c < nch; c += wpr) {
+                for (int q = 0; q < 4; ++q) {
+                    for (int s = 0; s < 32; ++s) {
+                        const uint64_t l = c * 128 + 32 * q + s;
+                        if (l >= W) continue;
+                        uint64_t jl = 0;
+                        const double dev = fm_walker(rec, nbr, thr, alias, i, l, T0, f0, corr_i,
+                                                     dt, inv_dt, n_grid, N, strang, k0, k1, &jl);
+                        b1[s] = b1[s] + dev;
+                        b2[s] = fma(dev, dev, b2[s]);
+                        bj[s] += jl;
+                    }
+                }
+            }
             for (int o = 16; o > 0; o >>= 1) {
                 double c1[32], c2[32];
                 uint64_t cj[32];
@@ -174,7 +194,7 @@ void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
                 memcpy(b2, c2, sizeof(c2));
                 memcpy(bj, cj, sizeof(cj));
             }
-            if (wbase == 0) { w1 = b1[0]; w2 = b2[0]; wj = bj[0]; }
+            if (wi == 0) { w1 = b1[0]; w2 = b2[0]; wj = bj[0]; }
             else { w1 = w1 + b1[0]; w2 = w2 + b2[0]; wj += bj[0]; }
         }
         const double Wd = (double)W;
@@ -188,7 +208,4 @@ void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
         se[r] = sev;
         jumps[r] = wj;
     }
-    free(a1);
-    free(a2);
-    free(aj);
 }

@@ -7,7 +7,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libexpmc_b200.so")
+# EXPMC_B200_LIB selects an alternative build of the same library (tuning
+# variants under paper_1904_12759_b200/variants/); default is the in-tree .so.
+LIB_PATH = os.environ.get("EXPMC_B200_LIB") or os.path.join(HERE, "libexpmc_b200.so")
 
 u64p = C.POINTER(C.c_uint64)
 u32p = C.POINTER(C.c_uint32)

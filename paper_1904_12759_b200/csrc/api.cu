@@ -139,7 +139,7 @@ struct expmc_matrix {
     DevSplit m;
     std::vector<void*> owned;
     DevBuf vdev, rows, out_val, out_se, out_j, fa, vcum, values, pa, pb, pc, scal, tmp1, tmp2,
-        tmp3, iota;
+        tmp3, iota, part;
     uint64_t iota_n = 0;
     // host copies kept for K5 norm bounds
     std::vector<double> h_rate, h_diag;
@@ -154,7 +154,7 @@ struct expmc_matrix {
     ~expmc_matrix() {
         for (void* p : owned) cudaFree(p);
         for (DevBuf* b : {&vdev, &rows, &out_val, &out_se, &out_j, &fa, &vcum, &values, &pa,
-                          &pb, &pc, &scal, &tmp1, &tmp2, &tmp3, &iota})
+                          &pb, &pc, &scal, &tmp1, &tmp2, &tmp3, &iota, &part})
             b->release();
         if (stream) cudaStreamDestroy(stream);
     }
@@ -162,9 +162,9 @@ struct expmc_matrix {
 
 namespace {
 
-cudaStream_t pick_stream(expmc_matrix* h, void* s) {
-    return s ? static_cast<cudaStream_t>(s) : h->stream;
-}
+// Device-API stream argument: a cudaStream_t; NULL is the legacy default
+// stream (CUDA's own convention), so torch's default stream handle works.
+cudaStream_t pick_stream(expmc_matrix*, void* s) { return static_cast<cudaStream_t>(s); }
 
 void check_vector(const expmc_matrix* h, const double* v, uint64_t nv) {
     // check_vector, estimator.cpp:130-139
@@ -285,6 +285,10 @@ expmc_matrix* build(uint64_t n, const uint64_t* row_ptr, const uint32_t* col, co
             h->tmp2.release();
             h->tmp3.release();
         }
+        m.adj = h->alloc<Edge>(nnz);
+        launch_build_adj(nnz, m.neighbor, m.rec, m.adj, s);
+        after_launch(nnz ? 1 : 0);
+        CK(cudaStreamSynchronize(s));
     } catch (...) {
         delete h;
         throw;
@@ -324,9 +328,13 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
     double* os = h->out_se.get<double>(nrows);
     uint64_t* oj = h->out_j.get<uint64_t>(nrows);
     if (p->rng == EXPMC_RNG_PHILOX) {
+        if (nrows >= (1ull << 30)) throw InvalidArg("at most 2^30 rows per call");
         launch_pack_v(n, vd, h->m.rec, s);
-        launch_entry_fast(h->m, rd, nrows, fast_params(p, p->samples), ov, os, oj, s);
-        after_launch(2);
+        launch_pack_v_adj(h->m.nnz, vd, h->m.adj, s);
+        void* scratch = h->part.get<unsigned char>(entry_fast_scratch_bytes(nrows, p->samples));
+        const int k = launch_entry_fast(h->m, rd, nrows, fast_params(p, p->samples), ov, os, oj,
+                                        scratch, s);
+        after_launch(2 + k);
     } else {
         const double dt = p->beta / (double)p->n_steps;
         const bool strang = p->splitting == EXPMC_STRANG;
@@ -652,7 +660,8 @@ int expmc_cuda_set_v_device(expmc_matrix* h, const double* v_dev, uint64_t nv, v
         CK(cudaStreamSynchronize(s));
         if (bad) throw InvalidArg("non-finite entry in v");
         launch_pack_v(nv, v_dev, h->m.rec, s);
-        after_launch(1);
+        launch_pack_v_adj(h->m.nnz, v_dev, h->m.adj, s);
+        after_launch(2);
     });
 }
 
@@ -666,10 +675,14 @@ int expmc_cuda_entries_device(expmc_matrix* h, const uint32_t* rows_dev, uint64_
             throw InvalidArg("entries_device supports the Philox walker only");
         if (p->samples >= (1ull << 32))
             throw InvalidArg("samples must be < 2^32 for the entry walker");
+        if (nrows >= (1ull << 30)) throw InvalidArg("at most 2^30 rows per call");
         DeviceGuard g(h->device);
-        launch_entry_fast(h->m, rows_dev, nrows, fast_params(p, p->samples), value_dev,
-                          std_error_dev, jumps_dev, pick_stream(h, stream));
-        after_launch(nrows ? 1 : 0);
+        // scratch is owned by the handle: one stream per handle at a time
+        void* scratch = h->part.get<unsigned char>(entry_fast_scratch_bytes(nrows, p->samples));
+        const int k = launch_entry_fast(h->m, rows_dev, nrows, fast_params(p, p->samples),
+                                        value_dev, std_error_dev, jumps_dev, scratch,
+                                        pick_stream(h, stream));
+        after_launch(k);
     });
 }
 

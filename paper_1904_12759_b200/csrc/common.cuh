@@ -24,6 +24,24 @@ struct __align__(32) RowRec {
 };
 static_assert(sizeof(RowRec) == 32, "RowRec must be one sector");
 
+// One 32-byte "fat" adjacency slot per directed edge (row i, column k):
+// everything a walker needs after jumping from i through column k — the
+// landing row j with its offset / degree / 1/rate / d and the current
+// call's v_j (refreshed by pack_v).  A jump on a uniform row is then ONE
+// dependent sector gather instead of neighbour-id -> row-record, and a
+// finished walker already holds its terminal score.  Weighted rows read
+// their alias entry (thr, alias arrays) first.  Costs nnz * 32 B of HBM
+// (5.1 GB for the largest configuration), which the 180 GB part affords.
+struct __align__(32) Edge {
+    uint32_t j;         // landing row
+    uint32_t off;       // its CSR offset
+    uint32_t deg_flags; // its degree | non-uniform flag
+    float inv_rate;     // its (float)(1/rate)
+    double d;           // its D_jj
+    double v;           // v_j of the current call
+};
+static_assert(sizeof(Edge) == 32, "Edge must be one sector");
+
 constexpr uint32_t kNonUniform = 0x80000000u;
 constexpr uint32_t kDegMask = 0x7fffffffu;
 
@@ -87,27 +105,30 @@ constexpr uint32_t kTagEntry = 0x454e5452u;  // 'ENTR'
 constexpr uint32_t kTagScatter = 0x56454354u; // 'VECT' (vector / tc)
 
 // -ln(u) for u = ((w >> 9) + 0.5) * 2^-23 in (0, 1), fp32, using only
-// IEEE-exact operations (fma, div) so the CPU model in oracle/fast_model.c
-// reproduces it bit for bit.  ln(m) = 2 atanh(s), s = (m-1)/(m+1),
-// m in [sqrt(1/2), sqrt(2)); |s| <= 0.1716, series to s^9 (rel. err < 3e-9).
+// IEEE-exact operations (mul, sub, fma) so the CPU model in
+// oracle/fast_model.c reproduces it bit for bit.  u = 2^e m with
+// m in [sqrt(1/2), sqrt(2)); ln(m) = f q(f), f = m - 1 (exact), q a degree-8
+// Chebyshev fit of log1p(f)/f on [sqrt(1/2)-1, sqrt(2)-1] (rel. err 2.7e-8).
 __device__ __forceinline__ float neg_ln_u(uint32_t w) {
     const float u = __fmul_rn(__uint2float_rn(w >> 9) + 0.5f, 0x1.0p-23f);
-    int e;
-    uint32_t bits = __float_as_uint(u);
-    e = (int)((bits >> 23) & 0xffu) - 127;
+    const uint32_t bits = __float_as_uint(u);
+    int e = (int)((bits >> 23) & 0xffu) - 127;
     float m = __uint_as_float((bits & 0x007fffffu) | 0x3f800000u);  // [1,2)
     if (m > 1.41421356f) {
         m = __fmul_rn(m, 0.5f);
         e += 1;
     }
-    const float s = __fdiv_rn(__fsub_rn(m, 1.0f), __fadd_rn(m, 1.0f));
-    const float z = __fmul_rn(s, s);
-    float p = __fmaf_rn(z, 0.11111111f, 0.14285715f);
-    p = __fmaf_rn(z, p, 0.2f);
-    p = __fmaf_rn(z, p, 0.33333334f);
-    p = __fmaf_rn(z, p, 1.0f);
-    const float lnm = __fmul_rn(__fmul_rn(2.0f, s), p);
-    const float ln_u = __fmaf_rn((float)e, 0.693147182f, lnm);
+    const float f = __fsub_rn(m, 1.0f);
+    float q = 0.08743945509195328f;
+    q = __fmaf_rn(q, f, -0.14377330243587494f);
+    q = __fmaf_rn(q, f, 0.14949095249176025f);
+    q = __fmaf_rn(q, f, -0.16560696065425873f);
+    q = __fmaf_rn(q, f, 0.19956977665424347f);
+    q = __fmaf_rn(q, f, -0.2500215470790863f);
+    q = __fmaf_rn(q, f, 0.3333418369293213f);
+    q = __fmaf_rn(q, f, -0.49999988079071045f);
+    q = __fmaf_rn(q, f, 1.0f);
+    const float ln_u = __fmaf_rn((float)e, 0.693147182f, __fmul_rn(f, q));
     return -ln_u;
 }
 
@@ -116,6 +137,62 @@ __device__ __forceinline__ uint32_t pick_index(uint32_t hi, uint32_t lo,
                                                uint32_t n) {
     const uint64_t x = ((uint64_t)hi << 32) | lo;
     return (uint32_t)__umul64hi(x, (uint64_t)n);
+}
+
+// One 32-byte row record through the read-only path (2 x 16-B loads of
+// the same sector).
+__device__ __forceinline__ RowRec load_rec(const RowRec* __restrict__ rec, uint32_t j) {
+    const int4* p = reinterpret_cast<const int4*>(rec + j);
+    const int4 a = __ldg(p);
+    const int4 b = __ldg(p + 1);
+    RowRec r;
+    r.off = (uint32_t)a.x;
+    r.deg_flags = (uint32_t)a.y;
+    r.inv_rate = __int_as_float(a.z);
+    r.spare = (uint32_t)a.w;
+    r.d = __hiloint2double(b.y, b.x);
+    r.v = __hiloint2double(b.w, b.z);
+    return r;
+}
+
+__device__ __forceinline__ Edge load_edge(const Edge* __restrict__ adj, uint32_t k) {
+    const int4* p = reinterpret_cast<const int4*>(adj + k);
+    const int4 a = __ldg(p);
+    const int4 b = __ldg(p + 1);
+    Edge e;
+    e.j = (uint32_t)a.x;
+    e.off = (uint32_t)a.y;
+    e.deg_flags = (uint32_t)a.z;
+    e.inv_rate = __int_as_float(a.w);
+    e.d = __hiloint2double(b.y, b.x);
+    e.v = __hiloint2double(b.w, b.z);
+    return e;
+}
+
+// Jump from the row (off, degf) through the fat adjacency: 64-bit pick
+// (hi, lo) of the column, alias correction with `coin` on weighted rows.
+__device__ __forceinline__ Edge jump_edge(uint32_t hi, uint32_t lo, uint32_t coin, uint32_t off,
+                                          uint32_t degf, const Edge* __restrict__ adj,
+                                          const uint32_t* __restrict__ thr,
+                                          const uint32_t* __restrict__ alias) {
+    uint32_t k = pick_index(hi, lo, degf & kDegMask);
+    if ((degf & kNonUniform) && coin >= __ldg(thr + off + k)) k = __ldg(alias + off + k);
+    return load_edge(adj, off + k);
+}
+
+// Landing row of a jump from the row (off, degf): uniform rows by degree
+// scaling (sampler.cpp:25-27) with a 64-bit draw (hi, lo), weighted rows by
+// the Walker alias table with the independent 32-bit coin.
+__device__ __forceinline__ uint32_t choose_next(uint32_t hi, uint32_t lo, uint32_t coin,
+                                                uint32_t off, uint32_t degf,
+                                                const uint32_t* __restrict__ nbr,
+                                                const uint32_t* __restrict__ thr,
+                                                const uint32_t* __restrict__ alias) {
+    uint32_t k = pick_index(hi, lo, degf & kDegMask);
+    if (degf & kNonUniform) {
+        if (coin >= __ldg(thr + off + k)) k = __ldg(alias + off + k);
+    }
+    return __ldg(nbr + off + k);
 }
 
 }  // namespace expmc_b200

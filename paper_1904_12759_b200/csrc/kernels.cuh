@@ -28,6 +28,7 @@ struct DevSplit {
     RowRec* rec = nullptr;       // n packed 32-B row records
     uint32_t* alias_thr = nullptr; // nnz (only if any_nonuniform)
     uint32_t* alias_idx = nullptr; // nnz (only if any_nonuniform)
+    Edge* adj = nullptr;           // nnz fat adjacency slots (32 B each)
 };
 
 // Parameters of the fast walkers (K3/K4).  Built once on the host from
@@ -55,6 +56,9 @@ void launch_alias_build(uint64_t n, const uint64_t* row_ptr, const double* weigh
                         uint32_t* alias, double* p, uint32_t* small, uint32_t* large,
                         cudaStream_t s);
 void launch_pack_v(uint64_t n, const double* v, RowRec* rec, cudaStream_t s);
+void launch_build_adj(uint64_t nnz, const uint32_t* neighbor, const RowRec* rec, Edge* adj,
+                      cudaStream_t s);
+void launch_pack_v_adj(uint64_t nnz, const double* v, Edge* adj, cudaStream_t s);
 void launch_node_factors(uint64_t n, const double* d, double scale, double* f,
                          cudaStream_t s);
 
@@ -71,9 +75,11 @@ void launch_scatter_compat(const DevSplit& m, int start_mode, const double* vcum
 
 // walk_fast.cu (K3, K4, K6)
 int entry_fast_wpr(uint64_t W);
-void launch_entry_fast(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
-                       const FastParams& p, double* value, double* se, uint64_t* jumps,
-                       cudaStream_t s);
+size_t entry_fast_scratch_bytes(uint64_t nrows, uint64_t W);
+// returns the number of kernels launched
+int launch_entry_fast(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
+                      const FastParams& p, double* value, double* se, uint64_t* jumps,
+                      void* scratch, cudaStream_t s);
 unsigned scatter_fast_grid();
 void launch_scatter_fast(const DevSplit& m, int start_mode, const double* vcum, double v_sum,
                          const FastParams& p, double* values, double* part_s1, double* part_s2,

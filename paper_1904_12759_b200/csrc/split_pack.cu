@@ -148,6 +148,44 @@ __global__ void alias_build_kernel(uint64_t n, const uint64_t* __restrict__ row_
     while (is < ns) { const uint32_t s = sm[is++]; th[s] = 0xffffffffu; al[s] = s; }
 }
 
+// Fat adjacency: one 32-B slot per directed edge (see Edge in common.cuh).
+// One thread per edge; coalesced stores, gathers of the landing record.
+__global__ void build_adj_kernel(uint64_t nnz, const uint32_t* __restrict__ neighbor,
+                                 const RowRec* __restrict__ rec, Edge* __restrict__ adj) {
+    const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (e >= nnz) return;
+    const uint32_t j = neighbor[e];
+    const RowRec r = rec[j];
+    Edge x;
+    x.j = j;
+    x.off = r.off;
+    x.deg_flags = r.deg_flags;
+    x.inv_rate = r.inv_rate;
+    x.d = r.d;
+    x.v = r.v;
+    adj[e] = x;
+}
+
+// Per call: refresh v_j in every fat-adjacency slot (8-B stores at a 32-B
+// stride, gathers of v from an L2-resident vector).
+__global__ void pack_v_adj_kernel(uint64_t nnz, const double* __restrict__ v,
+                                  Edge* __restrict__ adj) {
+    const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (e >= nnz) return;
+    adj[e].v = __ldg(v + adj[e].j);
+}
+
+void launch_build_adj(uint64_t nnz, const uint32_t* neighbor, const RowRec* rec, Edge* adj,
+                      cudaStream_t s) {
+    if (nnz == 0) return;
+    build_adj_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(nnz, neighbor, rec, adj);
+}
+
+void launch_pack_v_adj(uint64_t nnz, const double* v, Edge* adj, cudaStream_t s) {
+    if (nnz == 0) return;
+    pack_v_adj_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(nnz, v, adj);
+}
+
 __global__ void pack_v_kernel(uint64_t n, const double* __restrict__ v, RowRec* __restrict__ rec) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i < n) rec[i].v = v[i];

@@ -1,0 +1,358 @@
+// K3 entry walker — production kernel for the batched entry estimator
+// (Theorem 1; reference entry_estimate, proj/src/estimator.cpp:169-206).
+//
+// Same law as the reference for every walker, re-designed for SIMT:
+//
+//  * Continuous clock (memorylessness): one exponential per
+//    sojourn; a sojourn in state s over grid time [t, t') credits d_s to every
+//    grid point k Δt inside it, half weights at k = 0 and k = N for Strang
+//    (run_path, estimator.cpp:26-39).  Cost O(1 + jumps) per walker.
+//  * Philox4x32-10 keyed by the seed.  Walker l of row i: its first holding
+//    time comes from a decision word shared 4-per-Philox-block
+//    (counter (0xffffffff, 128c + (l mod 32), i, 'ENTR'), word (l mod 128)/32,
+//    c = l / 128); its j-th jump draws counter (j, l, i, 'ENTR'): words y,w =
+//    64-bit neighbour pick, z = alias coin, x = next holding time.  Randomness
+//    is a pure function of (seed, row, walker).
+//  * Walkers that never jump (decision word < 2^32 e^{-rate_i β}) score the
+//    deterministic f0 = e^{β d_i} v_i; sums are kept as deviations from f0, so
+//    they contribute exact zeros and cost 1/4 of a Philox block.
+//  * One dependent 32-B gather per jump through the fat adjacency (Edge).
+//  * Warp-cooperative scheduling over a stream of tasks.  Task t = (row
+//    t / WPR, part t % WPR) owns the row's chunks c ≡ part (mod WPR) of 128
+//    walkers.  A warp sweeps chunks (one Philox block per lane), pushes the
+//    jumpers as tickets into a shared-memory FIFO and idle lanes pop tickets,
+//    across task boundaries, so the sojourn code runs with full warps and a
+//    row's tail overlaps the next row's start.  A finished walker parks its
+//    log-weight and end row in its chunk slot; chunks are finalized strictly
+//    in order: exp() convergently over the chunk's jumpers, then lane s adds
+//    slots s, s+32, s+64, s+96.
+//  * Fixed accumulation order (result contract, replayed by
+//    oracle/fast_model.c): lane s of part w of a row sums the walkers
+//    l ≡ s (mod 32) with floor(l/128) ≡ w (mod WPR) in increasing l; lanes are
+//    combined by an xor butterfly, parts in index order.  Independent of
+//    scheduling, grid shape, GPU count and row sharding.
+#include "kernels.cuh"
+
+namespace expmc_b200 {
+
+namespace {
+
+constexpr int kChunk = 128;
+constexpr unsigned FULL = 0xffffffffu;
+
+struct RowConst {    // per task: the start row and its constants
+    RowRec rr;       // record of the row
+    double f0;       // e^{β d_i} v_i
+    double corr;     // weight correction at the start state
+    unsigned long long T0;  // never-jump threshold on a u32 draw
+    uint32_t i;      // matrix row
+    uint32_t pad;
+};
+
+struct ChunkMeta {
+    RowConst row;
+    uint32_t chunk;         // chunk index within the row
+    uint32_t tstart, tend;  // the chunk's ticket range
+    uint32_t task;          // task id
+    uint32_t last;          // last chunk of its task
+    uint32_t jumps;         // jumps of the chunk's finished walkers
+};
+
+template <int R>
+struct WarpRing {
+    double fx[R][kChunk];       // 0 for non-jumpers; log-weight, then f - f0
+    double fv[R][kChunk];       // v at the end state of a finished jumper
+    uint32_t dw[R][kChunk];     // decision word (first holding time)
+    uint16_t fifo[R * kChunk];  // tickets (ring slot << 7 | chunk slot)
+    ChunkMeta meta[R];
+    RowConst adm;               // row of the task being admitted
+};
+
+#ifndef ENTRY_MIN_BLOCKS
+#define ENTRY_MIN_BLOCKS 8
+#endif
+#ifndef ENTRY_RING
+#define ENTRY_RING 2
+#endif
+
+template <int WPR, int R>
+__global__ void __launch_bounds__(128, ENTRY_MIN_BLOCKS)
+entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rate,
+                  const Edge* __restrict__ adj, const uint32_t* __restrict__ thr,
+                  const uint32_t* __restrict__ alias, const uint32_t* __restrict__ rows,
+                  uint64_t nrows, FastParams p, double* __restrict__ out_value,
+                  double* __restrict__ out_se, uint64_t* __restrict__ out_jumps,
+                  double4* __restrict__ partial) {
+    constexpr uint32_t CAP = R * kChunk;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    __shared__ WarpRing<R> rings[4];
+    WarpRing<R>& q = rings[warp];
+    const uint32_t nch = (uint32_t)((p.W + kChunk - 1) / kChunk);
+    const uint64_t ntask = nrows * WPR;
+    const uint64_t tstride = (uint64_t)gridDim.x * 4;
+
+    // admission cursor (warp-uniform); the task's row constants live in smem
+    uint64_t atask = blockIdx.x * 4ull + warp;
+    uint32_t achunk = 0;
+    auto load_task = [&](uint64_t t) {
+        achunk = (uint32_t)(t % WPR);
+        if (lane == 0) {
+            RowConst& a = q.adm;
+            const uint32_t i = rows[t / WPR];
+            const RowRec ri = load_rec(rec, i);
+            const double p0 = exp(-__dmul_rn(__ldg(rate + i), p.beta));
+            a.rr = ri;
+            a.i = i;
+            a.T0 = (unsigned long long)__dmul_rn(p0, 4294967296.0);
+            a.f0 = __dmul_rn(exp(__dmul_rn(p.beta, ri.d)), ri.v);
+            a.corr = p.strang ? __dmul_rn(0.5, ri.d) : ri.d;
+        }
+        __syncwarp();
+    };
+    if (atask < ntask) load_task(atask);
+
+    int oldest = 0, live = 0;
+    uint32_t head = 0, tail = 0;
+    // lane-private walker state
+    bool act = false;
+    uint32_t myr = 0, slot = 0, l = 0, off = 0, degf = 0, G = 0, jc = 0, ew = 0;
+    float ir = 0.f;
+    double dcur = 0.0, vcur = 0.0, t = 0.0, S = 0.0;
+    // per-task accumulators (tasks finalize in order)
+    double s1 = 0.0, s2 = 0.0;
+    unsigned long long jsum = 0;
+
+    while (true) {
+        const unsigned idle = __ballot_sync(FULL, !act);
+        // ---- admit: sweep chunks while queued tickets cannot feed idle lanes
+        while (live < R && atask < ntask && tail - head < (uint32_t)__popc(idle)) {
+            const int rs = (oldest + live) % R;
+            const uint32_t base = achunk * kChunk;
+            const uint64_t T0 = q.adm.T0;
+            const U4 D = philox4x32_10(U4{0xffffffffu, base + (uint32_t)lane, q.adm.i, kTagEntry},
+                                       p.k0, p.k1);
+            const uint32_t wd[4] = {D.x, D.y, D.z, D.w};
+            const uint32_t t0 = tail;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const uint32_t sl = 32u * qq + lane;
+                const bool jmp = (uint64_t)(base + sl) < p.W && (uint64_t)wd[qq] >= T0;
+                q.fx[rs][sl] = 0.0;
+                if (jmp) q.dw[rs][sl] = wd[qq];
+                const unsigned b = __ballot_sync(FULL, jmp);
+                if (jmp) q.fifo[(tail + __popc(b & lt)) % CAP] = (uint16_t)((rs << 7) | sl);
+                tail += __popc(b);
+            }
+            const uint32_t nextc = achunk + WPR;
+            if (lane == 0) {
+                ChunkMeta& m = q.meta[rs];
+                m.row = q.adm;
+                m.chunk = achunk;
+                m.tstart = t0;
+                m.tend = tail;
+                m.task = (uint32_t)atask;
+                m.last = nextc >= nch;
+                m.jumps = 0;
+            }
+            __syncwarp();
+            ++live;
+            if (nextc < nch) {
+                achunk = nextc;
+            } else {
+                atask += tstride;
+                if (atask < ntask) load_task(atask);
+            }
+        }
+        // ---- pop: idle lanes take tickets in FIFO order
+        {
+            const uint32_t avail = tail - head;
+            const uint32_t nidle = (uint32_t)__popc(idle);
+            const uint32_t take = avail < nidle ? avail : nidle;
+            const uint32_t rank = (uint32_t)__popc(idle & lt);
+            if (!act && rank < take) {
+                const uint32_t tk = q.fifo[(head + rank) % CAP];
+                myr = tk >> 7;
+                slot = tk & 127u;
+                const ChunkMeta& m = q.meta[myr];
+                l = m.chunk * kChunk + slot;
+                off = m.row.rr.off; degf = m.row.rr.deg_flags;
+                ir = m.row.rr.inv_rate; dcur = m.row.rr.d; vcur = m.row.rr.v;
+                ew = q.dw[myr][slot];
+                t = 0.0; S = 0.0; G = 0; jc = 0;
+                act = true;
+            }
+            head += take;
+        }
+        // ---- one sojourn for every active lane
+        bool fin = false;
+        if (act) {
+            const float h = __fmul_rn(neg_ln_u(ew), ir);
+            const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
+            if (tn >= p.n_grid) {
+                S = __fma_rn(dcur, (double)(p.N + 1 - G), S);
+                const double c0 = q.meta[myr].row.corr;
+                const double c = p.strang ? __dadd_rn(c0, __dmul_rn(0.5, dcur)) : c0;
+                q.fx[myr][slot] = __dmul_rn(p.dt, __dsub_rn(S, c));
+                q.fv[myr][slot] = vcur;
+                act = false;
+                fin = true;
+            } else {
+                const uint32_t kk = (uint32_t)ceil(tn);
+                S = __fma_rn(dcur, (double)(kk - G), S);
+                G = kk;
+                t = tn;
+                const U4 B = philox4x32_10(U4{jc, l, q.meta[myr].row.i, kTagEntry}, p.k0, p.k1);
+                const Edge e = jump_edge(B.y, B.w, B.z, off, degf, adj, thr, alias);
+                off = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d; vcur = e.v;
+                ew = B.x;
+                ++jc;
+            }
+        }
+        // jumps of finished walkers, per chunk (warp reduction, no atomics)
+        if (__any_sync(FULL, fin)) {
+            for (int k = 0; k < live; ++k) {
+                const int rr = (oldest + k) % R;
+                const bool mine = fin && myr == (uint32_t)rr;
+                if (__any_sync(FULL, mine)) {
+                    const unsigned sj = __reduce_add_sync(FULL, mine ? jc : 0u);
+                    if (lane == 0) q.meta[rr].jumps += sj;
+                }
+            }
+        }
+        __syncwarp();
+        // ---- finalize the oldest chunks once all their walkers are done
+        while (live > 0 && (int)(head - q.meta[oldest].tend) >= 0 &&
+               __ballot_sync(FULL, act && myr == (uint32_t)oldest) == 0) {
+            const ChunkMeta& m = q.meta[oldest];
+            const uint32_t ts = m.tstart, te = m.tend;
+            const double f0 = m.row.f0;
+            for (uint32_t k = lane; k < te - ts; k += 32) {
+                const uint32_t sl = q.fifo[(ts + k) % CAP] & 127u;
+                q.fx[oldest][sl] = __dsub_rn(__dmul_rn(exp(q.fx[oldest][sl]), q.fv[oldest][sl]), f0);
+            }
+            __syncwarp();
+            const uint64_t base = (uint64_t)m.chunk * kChunk;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const uint32_t sl = 32u * qq + lane;
+                if (base + sl < p.W) {
+                    const double dev = q.fx[oldest][sl];
+                    s1 = __dadd_rn(s1, dev);
+                    s2 = __fma_rn(dev, dev, s2);
+                }
+            }
+            jsum += m.jumps;  // warp-uniform value
+            if (m.last) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    s1 = __dadd_rn(s1, __shfl_xor_sync(FULL, s1, o));
+                    s2 = __dadd_rn(s2, __shfl_xor_sync(FULL, s2, o));
+                }
+                if (lane == 0) {
+                    const uint64_t task = m.task;
+                    if (WPR == 1) {
+                        const double W = (double)p.W;
+                        out_value[task] = __dadd_rn(f0, __ddiv_rn(s1, W));
+                        double se = 0.0;
+                        if (p.W > 1) {
+                            double var =
+                                __ddiv_rn(__dsub_rn(s2, __ddiv_rn(__dmul_rn(s1, s1), W)),
+                                          __dsub_rn(W, 1.0));
+                            var = var > 0.0 ? var : 0.0;
+                            se = sqrt(__ddiv_rn(var, W));
+                        }
+                        out_se[task] = se;
+                        out_jumps[task] = jsum;
+                    } else {
+                        partial[task] = make_double4(s1, s2, __longlong_as_double((long long)jsum),
+                                                     f0);
+                    }
+                }
+                s1 = 0.0;
+                s2 = 0.0;
+                jsum = 0;
+            }
+            __syncwarp();
+            oldest = (oldest + 1) % R;
+            --live;
+        }
+        if (live == 0 && atask >= ntask) break;  // every chunk of every task finalized
+    }
+}
+
+// WPR > 1: combine the parts of each row in index order (same tree as the
+// contract: part 0, then += part 1, ...).
+template <int WPR>
+__global__ void combine_parts_kernel(const double4* __restrict__ partial, uint64_t nrows,
+                                     uint64_t W, double* __restrict__ out_value,
+                                     double* __restrict__ out_se, uint64_t* __restrict__ out_jumps) {
+    const uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (r >= nrows) return;
+    const double4 a = partial[r * WPR];
+    double s1 = a.x, s2 = a.y;
+    unsigned long long js = (unsigned long long)__double_as_longlong(a.z);
+    const double f0 = a.w;
+#pragma unroll
+    for (int k = 1; k < WPR; ++k) {
+        const double4 b = partial[r * WPR + k];
+        s1 = __dadd_rn(s1, b.x);
+        s2 = __dadd_rn(s2, b.y);
+        js += (unsigned long long)__double_as_longlong(b.z);
+    }
+    const double Wd = (double)W;
+    out_value[r] = __dadd_rn(f0, __ddiv_rn(s1, Wd));
+    double se = 0.0;
+    if (W > 1) {
+        double var = __ddiv_rn(__dsub_rn(s2, __ddiv_rn(__dmul_rn(s1, s1), Wd)), __dsub_rn(Wd, 1.0));
+        var = var > 0.0 ? var : 0.0;
+        se = sqrt(__ddiv_rn(var, Wd));
+    }
+    out_se[r] = se;
+    out_jumps[r] = js;
+}
+
+template <int WPR, int R>
+int launch_t(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const FastParams& p,
+             double* value, double* se, uint64_t* jumps, double4* partial, cudaStream_t s) {
+    const uint64_t warps = nrows * WPR;
+    const uint64_t blocks = (warps + 3) / 4;
+    const uint64_t cap = 148ull * ENTRY_MIN_BLOCKS;  // one wave of resident blocks
+    const unsigned grid = (unsigned)(blocks < cap ? blocks : cap);
+    entry_walk_kernel<WPR, R><<<grid, 128, 0, s>>>(m.rec, m.rate, m.adj, m.alias_thr, m.alias_idx,
+                                                   rows, nrows, p, value, se, jumps, partial);
+    if (WPR > 1) {
+        combine_parts_kernel<WPR><<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(
+            partial, nrows, p.W, value, se, jumps);
+        return 2;
+    }
+    return 1;
+}
+
+}  // namespace
+
+// Warps (parts) per row: a function of W only (part of the result contract).
+int entry_fast_wpr(uint64_t W) {
+    const uint64_t nch = (W + kChunk - 1) / kChunk;
+    return nch >= 64 ? 4 : (nch >= 32 ? 2 : 1);
+}
+
+size_t entry_fast_scratch_bytes(uint64_t nrows, uint64_t W) {
+    const int wpr = entry_fast_wpr(W);
+    return wpr > 1 ? nrows * (size_t)wpr * sizeof(double4) : 0;
+}
+
+int launch_entry_fast(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
+                      const FastParams& p, double* value, double* se, uint64_t* jumps,
+                      void* scratch, cudaStream_t s) {
+    if (nrows == 0) return 0;
+    double4* part = static_cast<double4*>(scratch);
+    switch (entry_fast_wpr(p.W)) {
+        case 4: return launch_t<4, ENTRY_RING>(m, rows, nrows, p, value, se, jumps, part, s);
+        case 2: return launch_t<2, ENTRY_RING>(m, rows, nrows, p, value, se, jumps, part, s);
+        default: return launch_t<1, ENTRY_RING>(m, rows, nrows, p, value, se, jumps, part, s);
+    }
+}
+
+}  // namespace expmc_b200

@@ -220,8 +220,10 @@ def entry_estimate(m: SplitMatrix, v, i: int, p: PathParams, workers: int = 1) -
     return Estimate(out.value, out.std_error, out.samples_used, out.total_jumps)
 
 
-def entries_estimate(m: SplitMatrix, v, rows, p: PathParams) -> EntriesEstimate:
-    """Batched entry_estimate: rows=None means every row (full vector)."""
+def entries_estimate(m: SplitMatrix, v, rows, p: PathParams, out=None) -> EntriesEstimate:
+    """Batched entry_estimate: rows=None means every row (full vector).
+    ``out`` = optional preallocated (values f64, std_errors f64, jumps u64)
+    host arrays (e.g. pinned) to write into."""
     v = _f64(v)
     pc = p._c()
     if rows is None:
@@ -235,7 +237,15 @@ def entries_estimate(m: SplitMatrix, v, rows, p: PathParams) -> EntriesEstimate:
         rows_arr = np.ascontiguousarray(rows_arr, dtype=np.uint32)
         nrows = len(rows_arr)
         rp = rows_arr.ctypes.data_as(u32p)
-    val, se, jm = np.zeros(nrows), np.zeros(nrows), np.zeros(nrows, np.uint64)
+    if out is None:
+        val, se, jm = np.zeros(nrows), np.zeros(nrows), np.zeros(nrows, np.uint64)
+    else:
+        val, se, jm = out
+        if not (len(val) >= nrows and len(se) >= nrows and len(jm) >= nrows
+                and val.dtype == np.float64 and se.dtype == np.float64
+                and jm.dtype in (np.uint64, np.int64) and val.flags.c_contiguous
+                and se.flags.c_contiguous and jm.flags.c_contiguous):
+            raise ValueError("out arrays must be contiguous f64/f64/u64 of length >= nrows")
     check(lib().expmc_cuda_entries(m.handle, v.ctypes.data_as(f64p), len(v), rp, nrows,
                                    C.byref(pc), val.ctypes.data_as(f64p),
                                    se.ctypes.data_as(f64p), jm.ctypes.data_as(u64p)))
