@@ -49,8 +49,9 @@ def gather_slices(value, se, jumps, nrows: int, group=None):
     packed[1, :k] = se
     packed[2, :k] = jumps.view(torch.float64) if jumps.dtype == torch.int64 else \
         jumps.to(torch.int64).view(torch.float64)
-    out = torch.empty(world, 3, width, dtype=torch.float64, device=dev)
-    dist.all_gather_into_tensor(out, packed, group=group)
+    flat = torch.empty(world * 3 * width, dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(flat, packed.reshape(-1), group=group)
+    out = flat.view(world, 3, width)
     vals, ses, js = [], [], []
     for r, (lo, hi) in enumerate(plan):
         m = hi - lo
