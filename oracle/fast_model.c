@@ -119,8 +119,10 @@ static double fm_walker(const fm_rec* rec, const uint32_t* nbr, const uint32_t* 
         const double tn = t + (double)h * inv_dt;
         if (tn >= n_grid) {
             S = fma(cur.d, (double)(N + 1 - g), S);
-            const double corr = strang ? corr_i + 0.5 * cur.d : corr_i;
-            const double x = dt * (S - corr);
+            /* the kernel parks S - d_end/2 (Strang) and forms the exponent
+             * at chunk finalize: x = dt * (S' - corr_i) */
+            const double Sp = strang ? S - 0.5 * cur.d : S;
+            const double x = dt * (Sp - corr_i);
             *jumps += jc;
             return exp(x) * cur.v - f0;
         }

@@ -128,6 +128,7 @@ FastParams fast_params(const expmc_path_params* p, uint64_t walkers) {
     f.W = walkers;
     f.k0 = (uint32_t)p->seed;
     f.k1 = (uint32_t)(p->seed >> 32);
+    f.rk = philox_keys(f.k0, f.k1);
     return f;
 }
 

@@ -101,6 +101,35 @@ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
     return c;
 }
 
+// Same function with a precomputed key schedule (kernel parameter / constant
+// bank): identical output, no per-thread registers for the 20 round keys.
+struct PhiloxKeys {
+    uint32_t k0[10], k1[10];
+};
+
+inline PhiloxKeys philox_keys(uint32_t k0, uint32_t k1) {
+    PhiloxKeys r;
+    for (int i = 0; i < 10; ++i) {
+        r.k0[i] = k0;
+        r.k1[i] = k1;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return r;
+}
+
+__device__ __forceinline__ U4 philox4x32_10(U4 c, const PhiloxKeys& K) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = U4{hi1 ^ c.y ^ K.k0[r], lo1, hi0 ^ c.w ^ K.k1[r], lo0};
+    }
+    return c;
+}
+
 constexpr uint32_t kTagEntry = 0x454e5452u;  // 'ENTR'
 constexpr uint32_t kTagScatter = 0x56454354u; // 'VECT' (vector / tc)
 
@@ -141,31 +170,42 @@ __device__ __forceinline__ uint32_t pick_index(uint32_t hi, uint32_t lo,
 
 // One 32-byte row record through the read-only path (2 x 16-B loads of
 // the same sector).
+__device__ __forceinline__ void ld256(const void* p, unsigned long long& a, unsigned long long& b,
+                                      unsigned long long& c, unsigned long long& d);
+
 __device__ __forceinline__ RowRec load_rec(const RowRec* __restrict__ rec, uint32_t j) {
-    const int4* p = reinterpret_cast<const int4*>(rec + j);
-    const int4 a = __ldg(p);
-    const int4 b = __ldg(p + 1);
+    unsigned long long a, b, c, d;
+    ld256(rec + j, a, b, c, d);
     RowRec r;
-    r.off = (uint32_t)a.x;
-    r.deg_flags = (uint32_t)a.y;
-    r.inv_rate = __int_as_float(a.z);
-    r.spare = (uint32_t)a.w;
-    r.d = __hiloint2double(b.y, b.x);
-    r.v = __hiloint2double(b.w, b.z);
+    r.off = (uint32_t)a;
+    r.deg_flags = (uint32_t)(a >> 32);
+    r.inv_rate = __uint_as_float((uint32_t)b);
+    r.spare = (uint32_t)(b >> 32);
+    r.d = __longlong_as_double((long long)c);
+    r.v = __longlong_as_double((long long)d);
     return r;
 }
 
+// One sector, one instruction: sm_100's 256-bit global load (SASS
+// LDG.E.ENL2.256) — a single L1 wavefront per gathered sector instead of
+// two 128-bit requests.
+__device__ __forceinline__ void ld256(const void* p, unsigned long long& a, unsigned long long& b,
+                                      unsigned long long& c, unsigned long long& d) {
+    asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+                 : "l"(p));
+}
+
 __device__ __forceinline__ Edge load_edge(const Edge* __restrict__ adj, uint32_t k) {
-    const int4* p = reinterpret_cast<const int4*>(adj + k);
-    const int4 a = __ldg(p);
-    const int4 b = __ldg(p + 1);
+    unsigned long long a, b, c, d;
+    ld256(adj + k, a, b, c, d);
     Edge e;
-    e.j = (uint32_t)a.x;
-    e.off = (uint32_t)a.y;
-    e.deg_flags = (uint32_t)a.z;
-    e.inv_rate = __int_as_float(a.w);
-    e.d = __hiloint2double(b.y, b.x);
-    e.v = __hiloint2double(b.w, b.z);
+    e.j = (uint32_t)a;
+    e.off = (uint32_t)(a >> 32);
+    e.deg_flags = (uint32_t)b;
+    e.inv_rate = __uint_as_float((uint32_t)(b >> 32));
+    e.d = __longlong_as_double((long long)c);
+    e.v = __longlong_as_double((long long)d);
     return e;
 }
 

@@ -42,6 +42,9 @@ struct FastParams {
     int strang;
     uint64_t W;    // walkers per entry (K3) or total walkers (K4)
     uint32_t k0, k1; // Philox key = seed
+    // Philox round keys (k0 + r W0, k1 + r W1), precomputed on the host so the
+    // rounds read them as constant-bank operands instead of registers.
+    PhiloxKeys rk;
 };
 
 // split_pack.cu

@@ -12,7 +12,8 @@
 //    (counter (0xffffffff, 128c + (l mod 32), i, 'ENTR'), word (l mod 128)/32,
 //    c = l / 128); its j-th jump draws counter (j, l, i, 'ENTR'): words y,w =
 //    64-bit neighbour pick, z = alias coin, x = next holding time.  Randomness
-//    is a pure function of (seed, row, walker).
+//    is a pure function of (seed, row, walker).  The block of jump j+1 is
+//    computed while the gather of jump j is in flight.
 //  * Walkers that never jump (decision word < 2^32 e^{-rate_i β}) score the
 //    deterministic f0 = e^{β d_i} v_i; sums are kept as deviations from f0, so
 //    they contribute exact zeros and cost 1/4 of a Philox block.
@@ -22,9 +23,10 @@
 //    walkers.  A warp sweeps chunks (one Philox block per lane), pushes the
 //    jumpers as tickets into a shared-memory FIFO and idle lanes pop tickets,
 //    across task boundaries, so the sojourn code runs with full warps and a
-//    row's tail overlaps the next row's start.  A finished walker parks its
-//    log-weight and end row in its chunk slot; chunks are finalized strictly
-//    in order: exp() convergently over the chunk's jumpers, then lane s adds
+//    row's tail overlaps the next row's start.  A finishing walker only parks
+//    its raw weight sum S, end value v and jump count in its chunk slot;
+//    chunks are finalized strictly in order: the weight, exp() and deviation
+//    are computed convergently over the chunk's jumpers, then lane s adds
 //    slots s, s+32, s+64, s+96.
 //  * Fixed accumulation order (result contract, replayed by
 //    oracle/fast_model.c): lane s of part w of a row sums the walkers
@@ -41,38 +43,43 @@ constexpr int kChunk = 128;
 constexpr unsigned FULL = 0xffffffffu;
 
 struct RowConst {    // per task: the start row and its constants
+    uint32_t i;      // matrix row            (i, chunk adjacent: one LDS.64)
+    uint32_t chunk;  // chunk index (ChunkMeta only)
+    unsigned long long T0;  // never-jump threshold on a u32 draw
     RowRec rr;       // record of the row
     double f0;       // e^{β d_i} v_i
-    double corr;     // weight correction at the start state
-    unsigned long long T0;  // never-jump threshold on a u32 draw
-    uint32_t i;      // matrix row
-    uint32_t pad;
+    double corr;     // weight correction at the start state (½ d_i Strang, d_i Lie)
 };
 
 struct ChunkMeta {
-    RowConst row;
-    uint32_t chunk;         // chunk index within the row
+    RowConst row;           // row.chunk = chunk index within the row
     uint32_t tstart, tend;  // the chunk's ticket range
     uint32_t task;          // task id
     uint32_t last;          // last chunk of its task
-    uint32_t jumps;         // jumps of the chunk's finished walkers
 };
 
 template <int R>
 struct WarpRing {
-    double fx[R][kChunk];       // 0 for non-jumpers; log-weight, then f - f0
-    double fv[R][kChunk];       // v at the end state of a finished jumper
-    uint32_t dw[R][kChunk];     // decision word (first holding time)
+    double fx[R][kChunk];   // 0 for non-jumpers; raw S at finish; then f - f0
+    double fv[R][kChunk];   // v at the end state of a finished jumper
+    uint32_t dw[R][kChunk]; // decision word until started; jump count at finish
     uint16_t fifo[R * kChunk];  // tickets (ring slot << 7 | chunk slot)
     ChunkMeta meta[R];
     RowConst adm;               // row of the task being admitted
 };
 
+// Tuning knobs (measured on B200, profiles/): 6 resident 128-thread blocks
+// per SM (80 registers, no hot-loop spills) beat 8 blocks at 64 registers;
+// computing the next Philox block ahead of the gather costs 4 registers and
+// loses (spills) — so it is off.
 #ifndef ENTRY_MIN_BLOCKS
-#define ENTRY_MIN_BLOCKS 8
+#define ENTRY_MIN_BLOCKS 6
 #endif
 #ifndef ENTRY_RING
 #define ENTRY_RING 2
+#endif
+#ifndef ENTRY_LOOKAHEAD
+#define ENTRY_LOOKAHEAD 0
 #endif
 
 template <int WPR, int R>
@@ -90,14 +97,14 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     __shared__ WarpRing<R> rings[4];
     WarpRing<R>& q = rings[warp];
     const uint32_t nch = (uint32_t)((p.W + kChunk - 1) / kChunk);
-    const uint64_t ntask = nrows * WPR;
-    const uint64_t tstride = (uint64_t)gridDim.x * 4;
+    const uint32_t ntask = (uint32_t)(nrows * WPR);
+    const uint32_t tstride = gridDim.x * 4u;
 
     // admission cursor (warp-uniform); the task's row constants live in smem
-    uint64_t atask = blockIdx.x * 4ull + warp;
+    uint32_t atask = blockIdx.x * 4u + warp;
     uint32_t achunk = 0;
-    auto load_task = [&](uint64_t t) {
-        achunk = (uint32_t)(t % WPR);
+    auto load_task = [&](uint32_t t) {
+        achunk = t % WPR;
         if (lane == 0) {
             RowConst& a = q.adm;
             const uint32_t i = rows[t / WPR];
@@ -117,9 +124,10 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     uint32_t head = 0, tail = 0;
     // lane-private walker state
     bool act = false;
-    uint32_t myr = 0, slot = 0, l = 0, off = 0, degf = 0, G = 0, jc = 0, ew = 0;
+    uint32_t tk = 0, off = 0, degf = 0, G = 0, jc = 0, ew = 0;
     float ir = 0.f;
     double dcur = 0.0, vcur = 0.0, t = 0.0, S = 0.0;
+    U4 B = U4{0, 0, 0, 0};  // Philox block of the walker's next jump
     // per-task accumulators (tasks finalize in order)
     double s1 = 0.0, s2 = 0.0;
     unsigned long long jsum = 0;
@@ -132,7 +140,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             const uint32_t base = achunk * kChunk;
             const uint64_t T0 = q.adm.T0;
             const U4 D = philox4x32_10(U4{0xffffffffu, base + (uint32_t)lane, q.adm.i, kTagEntry},
-                                       p.k0, p.k1);
+                                       p.rk);
             const uint32_t wd[4] = {D.x, D.y, D.z, D.w};
             const uint32_t t0 = tail;
 #pragma unroll
@@ -149,12 +157,11 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             if (lane == 0) {
                 ChunkMeta& m = q.meta[rs];
                 m.row = q.adm;
-                m.chunk = achunk;
+                m.row.chunk = achunk;
                 m.tstart = t0;
                 m.tend = tail;
-                m.task = (uint32_t)atask;
+                m.task = atask;
                 m.last = nextc >= nch;
-                m.jumps = 0;
             }
             __syncwarp();
             ++live;
@@ -172,68 +179,73 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             const uint32_t take = avail < nidle ? avail : nidle;
             const uint32_t rank = (uint32_t)__popc(idle & lt);
             if (!act && rank < take) {
-                const uint32_t tk = q.fifo[(head + rank) % CAP];
-                myr = tk >> 7;
-                slot = tk & 127u;
-                const ChunkMeta& m = q.meta[myr];
-                l = m.chunk * kChunk + slot;
+                tk = q.fifo[(head + rank) % CAP];
+                const ChunkMeta& m = q.meta[tk >> 7];
+                const uint32_t slot = tk & 127u;
                 off = m.row.rr.off; degf = m.row.rr.deg_flags;
                 ir = m.row.rr.inv_rate; dcur = m.row.rr.d; vcur = m.row.rr.v;
-                ew = q.dw[myr][slot];
+                ew = q.dw[tk >> 7][slot];
                 t = 0.0; S = 0.0; G = 0; jc = 0;
+#if ENTRY_LOOKAHEAD
+                B = philox4x32_10(U4{0u, m.row.chunk * kChunk + slot, m.row.i, kTagEntry},
+                                  p.rk);
+#endif
                 act = true;
             }
             head += take;
         }
         // ---- one sojourn for every active lane
-        bool fin = false;
         if (act) {
             const float h = __fmul_rn(neg_ln_u(ew), ir);
             const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
             if (tn >= p.n_grid) {
+                // park the raw weight sum; the exponent is formed at finalize
                 S = __fma_rn(dcur, (double)(p.N + 1 - G), S);
-                const double c0 = q.meta[myr].row.corr;
-                const double c = p.strang ? __dadd_rn(c0, __dmul_rn(0.5, dcur)) : c0;
-                q.fx[myr][slot] = __dmul_rn(p.dt, __dsub_rn(S, c));
-                q.fv[myr][slot] = vcur;
+                const uint32_t r = tk >> 7, sl = tk & 127u;
+                q.fx[r][sl] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, dcur)) : S;
+                q.fv[r][sl] = vcur;
+                q.dw[r][sl] = jc;
                 act = false;
-                fin = true;
             } else {
                 const uint32_t kk = (uint32_t)ceil(tn);
                 S = __fma_rn(dcur, (double)(kk - G), S);
                 G = kk;
                 t = tn;
-                const U4 B = philox4x32_10(U4{jc, l, q.meta[myr].row.i, kTagEntry}, p.k0, p.k1);
+#if !ENTRY_LOOKAHEAD
+                {
+                    const ChunkMeta& m = q.meta[tk >> 7];
+                    B = philox4x32_10(
+                        U4{jc, m.row.chunk * kChunk + (tk & 127u), m.row.i, kTagEntry}, p.rk);
+                }
+#endif
                 const Edge e = jump_edge(B.y, B.w, B.z, off, degf, adj, thr, alias);
-                off = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d; vcur = e.v;
                 ew = B.x;
                 ++jc;
-            }
-        }
-        // jumps of finished walkers, per chunk (warp reduction, no atomics)
-        if (__any_sync(FULL, fin)) {
-            for (int k = 0; k < live; ++k) {
-                const int rr = (oldest + k) % R;
-                const bool mine = fin && myr == (uint32_t)rr;
-                if (__any_sync(FULL, mine)) {
-                    const unsigned sj = __reduce_add_sync(FULL, mine ? jc : 0u);
-                    if (lane == 0) q.meta[rr].jumps += sj;
-                }
+#if ENTRY_LOOKAHEAD
+                // next block while the gather is in flight
+                const ChunkMeta& m = q.meta[tk >> 7];
+                B = philox4x32_10(U4{jc, m.row.chunk * kChunk + (tk & 127u), m.row.i, kTagEntry},
+                                  p.rk);
+#endif
+                off = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d; vcur = e.v;
             }
         }
         __syncwarp();
         // ---- finalize the oldest chunks once all their walkers are done
         while (live > 0 && (int)(head - q.meta[oldest].tend) >= 0 &&
-               __ballot_sync(FULL, act && myr == (uint32_t)oldest) == 0) {
+               __ballot_sync(FULL, act && (tk >> 7) == (uint32_t)oldest) == 0) {
             const ChunkMeta& m = q.meta[oldest];
             const uint32_t ts = m.tstart, te = m.tend;
-            const double f0 = m.row.f0;
+            const double f0 = m.row.f0, corr = m.row.corr;
+            unsigned long long jl = 0;
             for (uint32_t k = lane; k < te - ts; k += 32) {
                 const uint32_t sl = q.fifo[(ts + k) % CAP] & 127u;
-                q.fx[oldest][sl] = __dsub_rn(__dmul_rn(exp(q.fx[oldest][sl]), q.fv[oldest][sl]), f0);
+                const double x = __dmul_rn(p.dt, __dsub_rn(q.fx[oldest][sl], corr));
+                q.fx[oldest][sl] = __dsub_rn(__dmul_rn(exp(x), q.fv[oldest][sl]), f0);
+                jl += q.dw[oldest][sl];
             }
             __syncwarp();
-            const uint64_t base = (uint64_t)m.chunk * kChunk;
+            const uint64_t base = (uint64_t)m.row.chunk * kChunk;
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
                 const uint32_t sl = 32u * qq + lane;
@@ -243,12 +255,13 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                     s2 = __fma_rn(dev, dev, s2);
                 }
             }
-            jsum += m.jumps;  // warp-uniform value
+            jsum += jl;
             if (m.last) {
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
                     s1 = __dadd_rn(s1, __shfl_xor_sync(FULL, s1, o));
                     s2 = __dadd_rn(s2, __shfl_xor_sync(FULL, s2, o));
+                    jsum += __shfl_xor_sync(FULL, jsum, o);
                 }
                 if (lane == 0) {
                     const uint64_t task = m.task;

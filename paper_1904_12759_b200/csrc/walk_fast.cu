@@ -36,7 +36,7 @@ scatter_fast_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj
         if (!active) {
             if (l >= p.W) break;
             const U4 ws = philox4x32_10(U4{0xffffffffu, (uint32_t)l, (uint32_t)(l >> 32),
-                                           kTagScatter}, p.k0, p.k1);
+                                           kTagScatter}, p.rk);
             uint32_t s;
             if (start_mode == 0) {
                 s = pick_index(ws.x, ws.y, (uint32_t)n);
@@ -59,7 +59,7 @@ scatter_fast_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj
             active = true;
         }
         const U4 w = philox4x32_10(U4{step, (uint32_t)l, (uint32_t)(l >> 32), kTagScatter},
-                                   p.k0, p.k1);
+                                   p.rk);
         const float h = __fmul_rn(neg_ln_u(w.x), ir);
         const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
         if (tn >= p.n_grid) {
