@@ -134,6 +134,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
 
     while (true) {
         const unsigned idle = __ballot_sync(FULL, !act);
+        if (idle) {  // scheduler work only when a lane is free
         // ---- admit: sweep chunks while queued tickets cannot feed idle lanes
         while (live < R && atask < ntask && tail - head < (uint32_t)__popc(idle)) {
             const int rs = (oldest + live) % R;
@@ -194,7 +195,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             }
             head += take;
         }
+        }  // idle
         // ---- one sojourn for every active lane
+        bool fin = false;
         if (act) {
             const float h = __fmul_rn(neg_ln_u(ew), ir);
             const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
@@ -206,6 +209,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 q.fv[r][sl] = vcur;
                 q.dw[r][sl] = jc;
                 act = false;
+                fin = true;
             } else {
                 const uint32_t kk = (uint32_t)ceil(tn);
                 S = __fma_rn(dcur, (double)(kk - G), S);
@@ -230,8 +234,11 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 off = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d; vcur = e.v;
             }
         }
-        __syncwarp();
         // ---- finalize the oldest chunks once all their walkers are done
+        // (the condition can only change in an iteration that popped a
+        // ticket or retired a walker)
+        if (!(idle | __ballot_sync(FULL, fin))) continue;
+        __syncwarp();
         while (live > 0 && (int)(head - q.meta[oldest].tend) >= 0 &&
                __ballot_sync(FULL, act && (tk >> 7) == (uint32_t)oldest) == 0) {
             const ChunkMeta& m = q.meta[oldest];

@@ -1,0 +1,69 @@
+#!/usr/bin/env python
+"""Accuracy leg (SURVEY §8c iii): per configuration, compare the Monte
+Carlo entry estimates (K3) with deterministic GPU references (K5):
+
+  x_exact = exp(beta A) v                 (scaled Taylor, fp64)
+  x_split = splitting product the MC samples, (e^{dtD/2} e^{-dtL} e^{dtD/2})^N v
+
+and report eps_split = |x_split - x_exact| (the method's bias, the paper's
+eps_1) next to eps_stat = |x_mc - x_split| (Monte Carlo error, eps_2, which
+must sit within a few standard errors) and the total |x_mc - x_exact|, as
+mean relative errors (sum|.| / sum|x|, robust to signed v).  Writes one JSON
+line per config.
+
+usage: python scripts/accuracy.py [--configs 1 2 3 4 5] [--scale S] [--rows K]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_1904_12759_b200 as pb  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", type=int, nargs="*", default=[1, 2, 3, 4, 5])
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--rows", type=int, default=100_000, help="max rows estimated per config")
+    ap.add_argument("--seed", type=int, default=3)
+    args = ap.parse_args()
+    for c in args.configs:
+        t0 = time.time()
+        cfg = pb.build_config(c, args.scale)
+        m = pb.split(cfg.csr)
+        rows = cfg.rows if cfg.rows is not None else np.arange(cfg.csr.n, dtype=np.uint32)
+        if len(rows) > args.rows:
+            rows = np.sort(np.random.default_rng(7).choice(rows, args.rows, replace=False)
+                           ).astype(np.uint32)
+        p = pb.PathParams(cfg.beta, cfg.n_steps, cfg.walkers, pb.Splitting.Strang, args.seed)
+        mc = pb.entries_estimate(m, cfg.v, rows, p)
+        x_exact = pb.expmv(m, cfg.v, cfg.beta)[rows]
+        x_split = pb.splitting_product(m, cfg.v, p)[rows]
+        den = np.abs(x_exact).sum()
+        z = (mc.values - x_split) / np.maximum(mc.std_errors, 1e-300)
+        finite = mc.std_errors > 0
+        out = {
+            "config": f"cfg{c}_{cfg.name}", "rows": int(len(rows)), "walkers": cfg.walkers,
+            "n_steps": cfg.n_steps, "beta": cfg.beta,
+            "eps_split_rel": float(np.abs(x_split - x_exact).sum() / den),
+            "eps_stat_rel": float(np.abs(mc.values - x_split).sum() / den),
+            "eps_total_rel": float(np.abs(mc.values - x_exact).sum() / den),
+            "mean_se_rel": float(mc.std_errors.sum() / den),
+            "z_vs_split": {"mean": float(z[finite].mean()) if finite.any() else 0.0,
+                           "var": float(z[finite].var()) if finite.any() else 0.0,
+                           "frac_abs_gt4": float((np.abs(z[finite]) > 4).mean())
+                           if finite.any() else 0.0},
+            "seconds": time.time() - t0,
+        }
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

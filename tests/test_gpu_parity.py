@@ -340,3 +340,14 @@ def test_results_invariant_to_row_sharding(pb, graphs):
         parts = [pb.entries_estimate(m, v, rows[lo:hi], p) for lo, hi in plan_shards(csr.n, world)]
         assert np.array_equal(np.concatenate([q.values for q in parts]), full.values)
         assert np.array_equal(np.concatenate([q.jumps for q in parts]), full.jumps)
+
+
+def test_cpp_header_api_runs(tmp_path, pb):
+    import subprocess
+
+    from test_host import _build_cpp_demo
+
+    exe = _build_cpp_demo(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "api_demo ok" in r.stdout

@@ -203,3 +203,18 @@ def test_bench_reference_arm_cpu(ref):
     for k in ("metric", "unit", "cpu_baseline", "e2e", "config", "higher_is_better"):
         assert k in line
     assert line["cpu_baseline"]["kind"] == "reference"
+
+
+def _build_cpp_demo(out_dir):
+    exe = os.path.join(str(out_dir), "api_demo")
+    lib_dir = os.path.join(ROOT, "paper_1904_12759_b200")
+    cmd = ["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "cpp", "api_demo.cpp"), "-L", lib_dir, "-lexpmc_b200",
+           f"-Wl,-rpath,{lib_dir}", "-o", exe]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_cpp_header_api_compiles_and_links(tmp_path, pb):
+    _build_cpp_demo(tmp_path)
