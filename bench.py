@@ -53,6 +53,63 @@ def parse():
 
 
 # ---------------------------------------------------------------- clocks
+class NvmlSampler:
+    """SM clock + throttle reasons sampled in-process through NVML during the
+    timed region.  Spawning `nvidia-smi -lms 100` perturbed short kernels
+    (5-25 ms per step of GPU idle, scripts/diag_steps.py), so sampling is
+    in-process and every `interval` s (default 0.25)."""
+
+    def __init__(self, device, interval=0.25):
+        import pynvml
+
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        self.interval = interval
+        self.samples = []
+        self.stop_ev = threading.Event()
+
+    def _sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.samples.append((sm, mx, rs))
+
+    def _run(self):
+        while not self.stop_ev.wait(self.interval):
+            self._sample()
+
+    def start(self):
+        self._sample()  # NVML initialised and warm before the timed region
+        self.samples.clear()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def stop(self):
+        self.stop_ev.set()
+        self.t.join(timeout=5)
+        if not self.samples:
+            self._sample()  # short region: one sample right at its end
+        nv = self.nv
+        names = {nv.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                 nv.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                 nv.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                 nv.nvmlClocksEventReasonSwPowerCap: "sw_power_cap",
+                 nv.nvmlClocksEventReasonHwPowerBrakeSlowdown: "hw_power_brake"}
+        reasons = sorted({n for _, _, r in self.samples for bit, n in names.items() if r & bit})
+        return {"sm_mhz": statistics.median(s for s, _, _ in self.samples),
+                "sm_max_mhz": max(m for _, m, _ in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": f"nvml every {self.interval}s"}
+
+
+def make_sampler(device):
+    try:
+        return NvmlSampler(device)
+    except Exception:
+        return ClockSampler(device)
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -264,14 +321,15 @@ def main():
                           se.data_ptr(), jm.data_ptr(), sp)
         if timed:
             evs[k][1].record(stream)
-            jtot.add_(jm.sum())
+        jtot.add_(jm.sum())  # warm-up runs it too (lazy module load)
         if world > 1:
             gather_slices(val, se, jm, len(rows_all))
 
     for k in range(Wm):
         step(K + k, False)
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
+    jtot.zero_()
+    clocks = make_sampler(local)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()

@@ -12,22 +12,23 @@
 //    (counter (0xffffffff, 128c + (l mod 32), i, 'ENTR'), word (l mod 128)/32,
 //    c = l / 128); its j-th jump draws counter (j, l, i, 'ENTR'): words y,w =
 //    64-bit neighbour pick, z = alias coin, x = next holding time.  Randomness
-//    is a pure function of (seed, row, walker).  The block of jump j+1 is
-//    computed while the gather of jump j is in flight.
+//    is a pure function of (seed, row, walker).
 //  * Walkers that never jump (decision word < 2^32 e^{-rate_i β}) score the
 //    deterministic f0 = e^{β d_i} v_i; sums are kept as deviations from f0, so
 //    they contribute exact zeros and cost 1/4 of a Philox block.
 //  * One dependent 32-B gather per jump through the fat adjacency (Edge).
 //  * Warp-cooperative scheduling over a stream of tasks.  Task t = (row
 //    t / WPR, part t % WPR) owns the row's chunks c ≡ part (mod WPR) of 128
-//    walkers.  A warp sweeps chunks (one Philox block per lane), pushes the
-//    jumpers as tickets into a shared-memory FIFO and idle lanes pop tickets,
-//    across task boundaries, so the sojourn code runs with full warps and a
-//    row's tail overlaps the next row's start.  A finishing walker only parks
-//    its raw weight sum S, end value v and jump count in its chunk slot;
-//    chunks are finalized strictly in order: the weight, exp() and deviation
-//    are computed convergently over the chunk's jumpers, then lane s adds
-//    slots s, s+32, s+64, s+96.
+//    walkers.  A warp sweeps chunks (one Philox block per lane) and appends
+//    the jumpers as tickets to a shared-memory ring of kCap tickets (up to
+//    kRing chunks in flight); idle lanes pop tickets in order, across chunk
+//    and row boundaries, so the sojourn code runs with (nearly) full warps.
+//    A finishing walker only parks its raw weight sum S, end value v and
+//    jump count in its ticket; chunks are finalized strictly in order: the
+//    exponent, exp() and deviation are computed convergently over the
+//    chunk's tickets, scattered to a 128-slot buffer, and lane s adds slots
+//    s, s+32, s+64, s+96 (non-jumper zeros skipped: adding +0.0 never
+//    changes such a sum).
 //  * Fixed accumulation order (result contract, replayed by
 //    oracle/fast_model.c): lane s of part w of a row sums the walkers
 //    l ≡ s (mod 32) with floor(l/128) ≡ w (mod WPR) in increasing l; lanes are
@@ -42,6 +43,16 @@ namespace {
 constexpr int kChunk = 128;
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef ENTRY_MIN_BLOCKS
+#define ENTRY_MIN_BLOCKS 6
+#endif
+#ifndef ENTRY_RING
+#define ENTRY_RING 8    // chunks in flight per warp (power of 2)
+#endif
+#ifndef ENTRY_CAP
+#define ENTRY_CAP 256   // jumper tickets in flight per warp (power of 2, >= 128)
+#endif
+
 struct RowConst {    // per task: the start row and its constants
     uint32_t i;      // matrix row            (i, chunk adjacent: one LDS.64)
     uint32_t chunk;  // chunk index (ChunkMeta only)
@@ -53,36 +64,23 @@ struct RowConst {    // per task: the start row and its constants
 
 struct ChunkMeta {
     RowConst row;           // row.chunk = chunk index within the row
-    uint32_t tstart, tend;  // the chunk's ticket range
+    uint32_t tstart, tend;  // the chunk's ticket range (counters)
     uint32_t task;          // task id
     uint32_t last;          // last chunk of its task
 };
 
-template <int R>
-struct WarpRing {
-    double fx[R][kChunk];   // 0 for non-jumpers; raw S at finish; then f - f0
-    double fv[R][kChunk];   // v at the end state of a finished jumper
-    uint32_t dw[R][kChunk]; // decision word until started; jump count at finish
-    uint16_t fifo[R * kChunk];  // tickets (ring slot << 7 | chunk slot)
+template <int R, int CAP>
+struct WarpState {
+    double S[CAP];      // per ticket: raw weight sum at finish, then f - f0
+    double v[CAP];      // per ticket: v at the end state
+    uint32_t w[CAP];    // per ticket: decision word until started, then jump count
+    uint16_t rs[CAP];   // per ticket: ring slot << 8 | chunk slot
+    double dev[kChunk]; // finalize scatter buffer (slot order)
     ChunkMeta meta[R];
-    RowConst adm;               // row of the task being admitted
+    RowConst adm;       // row of the task being admitted
 };
 
-// Tuning knobs (measured on B200, profiles/): 6 resident 128-thread blocks
-// per SM (80 registers, no hot-loop spills) beat 8 blocks at 64 registers;
-// computing the next Philox block ahead of the gather costs 4 registers and
-// loses (spills) — so it is off.
-#ifndef ENTRY_MIN_BLOCKS
-#define ENTRY_MIN_BLOCKS 6
-#endif
-#ifndef ENTRY_RING
-#define ENTRY_RING 2
-#endif
-#ifndef ENTRY_LOOKAHEAD
-#define ENTRY_LOOKAHEAD 0
-#endif
-
-template <int WPR, int R>
+template <int WPR>
 __global__ void __launch_bounds__(128, ENTRY_MIN_BLOCKS)
 entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rate,
                   const Edge* __restrict__ adj, const uint32_t* __restrict__ thr,
@@ -90,12 +88,14 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                   uint64_t nrows, FastParams p, double* __restrict__ out_value,
                   double* __restrict__ out_se, uint64_t* __restrict__ out_jumps,
                   double4* __restrict__ partial) {
-    constexpr uint32_t CAP = R * kChunk;
+    constexpr int R = ENTRY_RING;
+    constexpr uint32_t CAP = ENTRY_CAP;
+    static_assert((R & (R - 1)) == 0 && (CAP & (CAP - 1)) == 0 && CAP >= kChunk, "ring sizes");
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
-    __shared__ WarpRing<R> rings[4];
-    WarpRing<R>& q = rings[warp];
+    __shared__ WarpState<R, CAP> states[4];
+    WarpState<R, CAP>& q = states[warp];
     const uint32_t nch = (uint32_t)((p.W + kChunk - 1) / kChunk);
     const uint32_t ntask = (uint32_t)(nrows * WPR);
     const uint32_t tstride = gridDim.x * 4u;
@@ -121,13 +121,12 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     if (atask < ntask) load_task(atask);
 
     int oldest = 0, live = 0;
-    uint32_t head = 0, tail = 0;
+    uint32_t head = 0, tail = 0;  // ticket counters (positions mod CAP)
     // lane-private walker state
     bool act = false;
-    uint32_t tk = 0, off = 0, degf = 0, G = 0, jc = 0, ew = 0;
+    uint32_t tk = 0, rsl = 0, off = 0, degf = 0, G = 0, jc = 0, ew = 0;
     float ir = 0.f;
     double dcur = 0.0, vcur = 0.0, t = 0.0, S = 0.0;
-    U4 B = U4{0, 0, 0, 0};  // Philox block of the walker's next jump
     // per-task accumulators (tasks finalize in order)
     double s1 = 0.0, s2 = 0.0;
     unsigned long long jsum = 0;
@@ -135,67 +134,66 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     while (true) {
         const unsigned idle = __ballot_sync(FULL, !act);
         if (idle) {  // scheduler work only when a lane is free
-        // ---- admit: sweep chunks while queued tickets cannot feed idle lanes
-        while (live < R && atask < ntask && tail - head < (uint32_t)__popc(idle)) {
-            const int rs = (oldest + live) % R;
-            const uint32_t base = achunk * kChunk;
-            const uint64_t T0 = q.adm.T0;
-            const U4 D = philox4x32_10(U4{0xffffffffu, base + (uint32_t)lane, q.adm.i, kTagEntry},
-                                       p.rk);
-            const uint32_t wd[4] = {D.x, D.y, D.z, D.w};
-            const uint32_t t0 = tail;
+            // ---- admit: sweep chunks while queued tickets cannot feed the
+            // idle lanes and a whole chunk's tickets fit in the ring
+            while (live < R && atask < ntask && tail - head < (uint32_t)__popc(idle) &&
+                   tail + kChunk - (live ? q.meta[oldest].tstart : tail) <= CAP) {
+                const int rs = (oldest + live) & (R - 1);
+                const uint32_t base = achunk * kChunk;
+                const uint64_t T0 = q.adm.T0;
+                const U4 D = philox4x32_10(
+                    U4{0xffffffffu, base + (uint32_t)lane, q.adm.i, kTagEntry}, p.rk);
+                const uint32_t wd[4] = {D.x, D.y, D.z, D.w};
+                const uint32_t t0 = tail;
 #pragma unroll
-            for (int qq = 0; qq < 4; ++qq) {
-                const uint32_t sl = 32u * qq + lane;
-                const bool jmp = (uint64_t)(base + sl) < p.W && (uint64_t)wd[qq] >= T0;
-                q.fx[rs][sl] = 0.0;
-                if (jmp) q.dw[rs][sl] = wd[qq];
-                const unsigned b = __ballot_sync(FULL, jmp);
-                if (jmp) q.fifo[(tail + __popc(b & lt)) % CAP] = (uint16_t)((rs << 7) | sl);
-                tail += __popc(b);
+                for (int qq = 0; qq < 4; ++qq) {
+                    const uint32_t sl = 32u * qq + lane;
+                    const bool jmp = (uint64_t)(base + sl) < p.W && (uint64_t)wd[qq] >= T0;
+                    const unsigned b = __ballot_sync(FULL, jmp);
+                    if (jmp) {
+                        const uint32_t pos = (tail + __popc(b & lt)) & (CAP - 1);
+                        q.w[pos] = wd[qq];
+                        q.rs[pos] = (uint16_t)((rs << 8) | sl);
+                    }
+                    tail += __popc(b);
+                }
+                const uint32_t nextc = achunk + WPR;
+                if (lane == 0) {
+                    ChunkMeta& m = q.meta[rs];
+                    m.row = q.adm;
+                    m.row.chunk = achunk;
+                    m.tstart = t0;
+                    m.tend = tail;
+                    m.task = atask;
+                    m.last = nextc >= nch;
+                }
+                __syncwarp();
+                ++live;
+                if (nextc < nch) {
+                    achunk = nextc;
+                } else {
+                    atask += tstride;
+                    if (atask < ntask) load_task(atask);
+                }
             }
-            const uint32_t nextc = achunk + WPR;
-            if (lane == 0) {
-                ChunkMeta& m = q.meta[rs];
-                m.row = q.adm;
-                m.row.chunk = achunk;
-                m.tstart = t0;
-                m.tend = tail;
-                m.task = atask;
-                m.last = nextc >= nch;
-            }
-            __syncwarp();
-            ++live;
-            if (nextc < nch) {
-                achunk = nextc;
-            } else {
-                atask += tstride;
-                if (atask < ntask) load_task(atask);
-            }
-        }
-        // ---- pop: idle lanes take tickets in FIFO order
-        {
+            // ---- pop: idle lanes take tickets in order
             const uint32_t avail = tail - head;
             const uint32_t nidle = (uint32_t)__popc(idle);
             const uint32_t take = avail < nidle ? avail : nidle;
             const uint32_t rank = (uint32_t)__popc(idle & lt);
             if (!act && rank < take) {
-                tk = q.fifo[(head + rank) % CAP];
-                const ChunkMeta& m = q.meta[tk >> 7];
-                const uint32_t slot = tk & 127u;
+                tk = head + rank;
+                const uint32_t pos = tk & (CAP - 1);
+                rsl = q.rs[pos];
+                const ChunkMeta& m = q.meta[rsl >> 8];
                 off = m.row.rr.off; degf = m.row.rr.deg_flags;
                 ir = m.row.rr.inv_rate; dcur = m.row.rr.d; vcur = m.row.rr.v;
-                ew = q.dw[tk >> 7][slot];
+                ew = q.w[pos];
                 t = 0.0; S = 0.0; G = 0; jc = 0;
-#if ENTRY_LOOKAHEAD
-                B = philox4x32_10(U4{0u, m.row.chunk * kChunk + slot, m.row.i, kTagEntry},
-                                  p.rk);
-#endif
                 act = true;
             }
             head += take;
         }
-        }  // idle
         // ---- one sojourn for every active lane
         bool fin = false;
         if (act) {
@@ -204,10 +202,10 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             if (tn >= p.n_grid) {
                 // park the raw weight sum; the exponent is formed at finalize
                 S = __fma_rn(dcur, (double)(p.N + 1 - G), S);
-                const uint32_t r = tk >> 7, sl = tk & 127u;
-                q.fx[r][sl] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, dcur)) : S;
-                q.fv[r][sl] = vcur;
-                q.dw[r][sl] = jc;
+                const uint32_t pos = tk & (CAP - 1);
+                q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, dcur)) : S;
+                q.v[pos] = vcur;
+                q.w[pos] = jc;
                 act = false;
                 fin = true;
             } else {
@@ -215,22 +213,12 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 S = __fma_rn(dcur, (double)(kk - G), S);
                 G = kk;
                 t = tn;
-#if !ENTRY_LOOKAHEAD
-                {
-                    const ChunkMeta& m = q.meta[tk >> 7];
-                    B = philox4x32_10(
-                        U4{jc, m.row.chunk * kChunk + (tk & 127u), m.row.i, kTagEntry}, p.rk);
-                }
-#endif
+                const ChunkMeta& m = q.meta[rsl >> 8];
+                const U4 B = philox4x32_10(
+                    U4{jc, m.row.chunk * kChunk + (rsl & 255u), m.row.i, kTagEntry}, p.rk);
                 const Edge e = jump_edge(B.y, B.w, B.z, off, degf, adj, thr, alias);
                 ew = B.x;
                 ++jc;
-#if ENTRY_LOOKAHEAD
-                // next block while the gather is in flight
-                const ChunkMeta& m = q.meta[tk >> 7];
-                B = philox4x32_10(U4{jc, m.row.chunk * kChunk + (tk & 127u), m.row.i, kTagEntry},
-                                  p.rk);
-#endif
                 off = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d; vcur = e.v;
             }
         }
@@ -239,27 +227,32 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         // ticket or retired a walker)
         if (!(idle | __ballot_sync(FULL, fin))) continue;
         __syncwarp();
-        while (live > 0 && (int)(head - q.meta[oldest].tend) >= 0 &&
-               __ballot_sync(FULL, act && (tk >> 7) == (uint32_t)oldest) == 0) {
+        while (live > 0) {
             const ChunkMeta& m = q.meta[oldest];
             const uint32_t ts = m.tstart, te = m.tend;
+            if ((int)(head - te) < 0 ||
+                __ballot_sync(FULL, act && tk - ts < te - ts) != 0)
+                break;
             const double f0 = m.row.f0, corr = m.row.corr;
+            const uint64_t base = (uint64_t)m.row.chunk * kChunk;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) q.dev[32 * qq + lane] = 0.0;
+            __syncwarp();
             unsigned long long jl = 0;
-            for (uint32_t k = lane; k < te - ts; k += 32) {
-                const uint32_t sl = q.fifo[(ts + k) % CAP] & 127u;
-                const double x = __dmul_rn(p.dt, __dsub_rn(q.fx[oldest][sl], corr));
-                q.fx[oldest][sl] = __dsub_rn(__dmul_rn(exp(x), q.fv[oldest][sl]), f0);
-                jl += q.dw[oldest][sl];
+            for (uint32_t k = ts + lane; k < te; k += 32) {
+                const uint32_t pos = k & (CAP - 1);
+                const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], corr));
+                q.dev[q.rs[pos] & 255u] = __dsub_rn(__dmul_rn(exp(x), q.v[pos]), f0);
+                jl += q.w[pos];
             }
             __syncwarp();
-            const uint64_t base = (uint64_t)m.row.chunk * kChunk;
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
                 const uint32_t sl = 32u * qq + lane;
                 if (base + sl < p.W) {
-                    const double dev = q.fx[oldest][sl];
-                    s1 = __dadd_rn(s1, dev);
-                    s2 = __fma_rn(dev, dev, s2);
+                    const double dv = q.dev[sl];
+                    s1 = __dadd_rn(s1, dv);
+                    s2 = __fma_rn(dv, dv, s2);
                 }
             }
             jsum += jl;
@@ -295,7 +288,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 jsum = 0;
             }
             __syncwarp();
-            oldest = (oldest + 1) % R;
+            oldest = (oldest + 1) & (R - 1);
             --live;
         }
         if (live == 0 && atask >= ntask) break;  // every chunk of every task finalized
@@ -333,15 +326,15 @@ __global__ void combine_parts_kernel(const double4* __restrict__ partial, uint64
     out_jumps[r] = js;
 }
 
-template <int WPR, int R>
+template <int WPR>
 int launch_t(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const FastParams& p,
              double* value, double* se, uint64_t* jumps, double4* partial, cudaStream_t s) {
     const uint64_t warps = nrows * WPR;
     const uint64_t blocks = (warps + 3) / 4;
     const uint64_t cap = 148ull * ENTRY_MIN_BLOCKS;  // one wave of resident blocks
     const unsigned grid = (unsigned)(blocks < cap ? blocks : cap);
-    entry_walk_kernel<WPR, R><<<grid, 128, 0, s>>>(m.rec, m.rate, m.adj, m.alias_thr, m.alias_idx,
-                                                   rows, nrows, p, value, se, jumps, partial);
+    entry_walk_kernel<WPR><<<grid, 128, 0, s>>>(m.rec, m.rate, m.adj, m.alias_thr, m.alias_idx,
+                                                rows, nrows, p, value, se, jumps, partial);
     if (WPR > 1) {
         combine_parts_kernel<WPR><<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(
             partial, nrows, p.W, value, se, jumps);
@@ -369,9 +362,9 @@ int launch_entry_fast(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
     if (nrows == 0) return 0;
     double4* part = static_cast<double4*>(scratch);
     switch (entry_fast_wpr(p.W)) {
-        case 4: return launch_t<4, ENTRY_RING>(m, rows, nrows, p, value, se, jumps, part, s);
-        case 2: return launch_t<2, ENTRY_RING>(m, rows, nrows, p, value, se, jumps, part, s);
-        default: return launch_t<1, ENTRY_RING>(m, rows, nrows, p, value, se, jumps, part, s);
+        case 4: return launch_t<4>(m, rows, nrows, p, value, se, jumps, part, s);
+        case 2: return launch_t<2>(m, rows, nrows, p, value, se, jumps, part, s);
+        default: return launch_t<1>(m, rows, nrows, p, value, se, jumps, part, s);
     }
 }
 
