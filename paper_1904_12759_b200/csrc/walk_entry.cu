@@ -131,7 +131,34 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     double s1 = 0.0, s2 = 0.0;
     unsigned long long jsum = 0;
 
+    // One sojourn of the lane's walker from its current state: either the
+    // path ends (park S', v, jumps in the ticket; lane becomes idle) or the
+    // grid points are credited and the walker must jump (`jmp`).
+    auto sojourn = [&](bool& fin, bool& jmp) {
+        const float h = __fmul_rn(neg_ln_u(ew), ir);
+        const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
+        if (tn >= p.n_grid) {
+            // park the raw weight sum; the exponent is formed at finalize
+            S = __fma_rn(dcur, (double)(p.N + 1 - G), S);
+            const uint32_t pos = tk & (CAP - 1);
+            q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, dcur)) : S;
+            q.v[pos] = vcur;
+            q.w[pos] = jc;
+            act = false;
+            fin = true;
+        } else {
+            const uint32_t kk = (uint32_t)ceil(tn);
+            S = __fma_rn(dcur, (double)(kk - G), S);
+            G = kk;
+            t = tn;
+            jmp = true;
+        }
+    };
+
     while (true) {
+        // ---- A: sojourn of every walker in flight
+        bool fin = false, jmp = false;
+        if (act) sojourn(fin, jmp);
         const unsigned idle = __ballot_sync(FULL, !act);
         if (idle) {  // scheduler work only when a lane is free
             // ---- admit: sweep chunks while queued tickets cannot feed the
@@ -191,36 +218,21 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 ew = q.w[pos];
                 t = 0.0; S = 0.0; G = 0; jc = 0;
                 act = true;
+                // a jumper's first sojourn ends in a jump (decision word >= T0),
+                // so it joins this iteration's jump
+                sojourn(fin, jmp);
             }
             head += take;
         }
-        // ---- one sojourn for every active lane
-        bool fin = false;
-        if (act) {
-            const float h = __fmul_rn(neg_ln_u(ew), ir);
-            const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
-            if (tn >= p.n_grid) {
-                // park the raw weight sum; the exponent is formed at finalize
-                S = __fma_rn(dcur, (double)(p.N + 1 - G), S);
-                const uint32_t pos = tk & (CAP - 1);
-                q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, dcur)) : S;
-                q.v[pos] = vcur;
-                q.w[pos] = jc;
-                act = false;
-                fin = true;
-            } else {
-                const uint32_t kk = (uint32_t)ceil(tn);
-                S = __fma_rn(dcur, (double)(kk - G), S);
-                G = kk;
-                t = tn;
-                const ChunkMeta& m = q.meta[rsl >> 8];
-                const U4 B = philox4x32_10(
-                    U4{jc, m.row.chunk * kChunk + (rsl & 255u), m.row.i, kTagEntry}, p.rk);
-                const Edge e = jump_edge(B.y, B.w, B.z, off, degf, adj, thr, alias);
-                ew = B.x;
-                ++jc;
-                off = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d; vcur = e.v;
-            }
+        // ---- C: one jump for every walker whose sojourn did not end the path
+        if (jmp) {
+            const ChunkMeta& m = q.meta[rsl >> 8];
+            const U4 B = philox4x32_10(
+                U4{jc, m.row.chunk * kChunk + (rsl & 255u), m.row.i, kTagEntry}, p.rk);
+            const Edge e = jump_edge(B.y, B.w, B.z, off, degf, adj, thr, alias);
+            ew = B.x;
+            ++jc;
+            off = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d; vcur = e.v;
         }
         // ---- finalize the oldest chunks once all their walkers are done
         // (the condition can only change in an iteration that popped a
