@@ -137,6 +137,8 @@ FastParams fast_params(const expmc_path_params* p, uint64_t walkers) {
 struct expmc_matrix {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // D2H of result pieces (host API)
+    cudaEvent_t piece_done = nullptr;
     DevSplit m;
     std::vector<void*> owned;
     DevBuf vdev, rows, out_val, out_se, out_j, fa, vcum, values, pa, pb, pc, scal, tmp1, tmp2,
@@ -158,6 +160,8 @@ struct expmc_matrix {
                           &pb, &pc, &scal, &tmp1, &tmp2, &tmp3, &iota, &part})
             b->release();
         if (stream) cudaStreamDestroy(stream);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (piece_done) cudaEventDestroy(piece_done);
     }
 };
 
@@ -205,6 +209,8 @@ expmc_matrix* build(uint64_t n, const uint64_t* row_ptr, const uint32_t* col, co
     try {
         h->device = device;
         CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h->piece_done, cudaEventDisableTiming));
         DevSplit& m = h->m;
         m.n = n;
         m.nnz = nnz;
@@ -302,7 +308,14 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
                  uint64_t nrows, const expmc_path_params* p, double* value, double* se,
                  uint64_t* jumps) {
     validate_params(p);
-    check_vector(h, v, nv);
+    const bool fast = p->rng == EXPMC_RNG_PHILOX;
+    if (fast) {
+        // length here; finiteness on the device (same message), so the host
+        // does not scan v on the critical path
+        if (nv != h->m.n || (!v && nv)) throw InvalidArg("vector length does not match matrix");
+    } else {
+        check_vector(h, v, nv);
+    }
     const uint64_t n = h->m.n;
     if (rows) {
         for (uint64_t r = 0; r < nrows; ++r)
@@ -310,13 +323,61 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
     } else if (nrows != n) {
         throw InvalidArg("rows == NULL requires nrows == n");
     }
-    if (p->rng == EXPMC_RNG_PHILOX && p->samples >= (1ull << 32))
+    if (fast && p->samples >= (1ull << 32))
         throw InvalidArg("samples must be < 2^32 for the entry walker");
     if (nrows == 0) return;
     DeviceGuard g(h->device);
     cudaStream_t s = h->stream;
     double* vd = h->vdev.get<double>(n);
     CK(cudaMemcpyAsync(vd, v, n * 8, cudaMemcpyHostToDevice, s));
+    if (fast) {
+        // E2E path: device finiteness check, then the rows in pieces whose
+        // results are copied back on a second stream while the next piece
+        // runs (the walker work of different rows is independent)
+        unsigned int* flag = h->scal.get<unsigned int>(4);
+        CK(cudaMemsetAsync(flag, 0, 4, s));
+        launch_count_nonfinite(n, vd, flag, s);
+        launch_pack_v(n, vd, h->m.rec, s);
+        launch_pack_v_adj(h->m.nnz, vd, h->m.adj, s);
+        after_launch(3);
+        if (nrows >= (1ull << 30)) throw InvalidArg("at most 2^30 rows per call");
+        const uint32_t* rd;
+        if (rows) {
+            uint32_t* r = h->rows.get<uint32_t>(nrows);
+            CK(cudaMemcpyAsync(r, rows, nrows * 4, cudaMemcpyHostToDevice, s));
+            rd = r;
+        } else {
+            rd = all_rows(h);
+        }
+        double* ov = h->out_val.get<double>(nrows);
+        double* os = h->out_se.get<double>(nrows);
+        uint64_t* oj = h->out_j.get<uint64_t>(nrows);
+        const uint64_t pieces = nrows >= (1ull << 20) ? 4 : 1;
+        void* scratch =
+            h->part.get<unsigned char>(entry_fast_scratch_bytes((nrows + pieces - 1) / pieces,
+                                                                p->samples));
+        const FastParams fp = fast_params(p, p->samples);
+        for (uint64_t k = 0; k < pieces; ++k) {
+            const uint64_t lo = nrows * k / pieces, hi = nrows * (k + 1) / pieces;
+            const int kl = launch_entry_fast(h->m, rd + lo, hi - lo, fp, ov + lo, os + lo, oj + lo,
+                                             scratch, s);
+            after_launch(kl);
+            CK(cudaEventRecord(h->piece_done, s));
+            CK(cudaStreamWaitEvent(h->copy_stream, h->piece_done, 0));
+            CK(cudaMemcpyAsync(value + lo, ov + lo, (hi - lo) * 8, cudaMemcpyDeviceToHost,
+                               h->copy_stream));
+            CK(cudaMemcpyAsync(se + lo, os + lo, (hi - lo) * 8, cudaMemcpyDeviceToHost,
+                               h->copy_stream));
+            CK(cudaMemcpyAsync(jumps + lo, oj + lo, (hi - lo) * 8, cudaMemcpyDeviceToHost,
+                               h->copy_stream));
+        }
+        unsigned int bad = 0;
+        CK(cudaMemcpyAsync(&bad, flag, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        CK(cudaStreamSynchronize(h->copy_stream));
+        if (bad) throw InvalidArg("non-finite entry in v");
+        return;
+    }
     const uint32_t* rd;
     if (rows) {
         uint32_t* r = h->rows.get<uint32_t>(nrows);
@@ -328,15 +389,7 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
     double* ov = h->out_val.get<double>(nrows);
     double* os = h->out_se.get<double>(nrows);
     uint64_t* oj = h->out_j.get<uint64_t>(nrows);
-    if (p->rng == EXPMC_RNG_PHILOX) {
-        if (nrows >= (1ull << 30)) throw InvalidArg("at most 2^30 rows per call");
-        launch_pack_v(n, vd, h->m.rec, s);
-        launch_pack_v_adj(h->m.nnz, vd, h->m.adj, s);
-        void* scratch = h->part.get<unsigned char>(entry_fast_scratch_bytes(nrows, p->samples));
-        const int k = launch_entry_fast(h->m, rd, nrows, fast_params(p, p->samples), ov, os, oj,
-                                        scratch, s);
-        after_launch(2 + k);
-    } else {
+    {  // PCG-compat parity walker
         const double dt = p->beta / (double)p->n_steps;
         const bool strang = p->splitting == EXPMC_STRANG;
         double* f = h->fa.get<double>(n);

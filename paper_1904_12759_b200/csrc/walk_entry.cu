@@ -52,6 +52,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef ENTRY_CAP
 #define ENTRY_CAP 256   // jumper tickets in flight per warp (power of 2, >= 128)
 #endif
+#ifndef ENTRY_POP_MIN
+#define ENTRY_POP_MIN 2 // run the scheduler once this many lanes are idle
+#endif
 
 struct RowConst {    // per task: the start row and its constants
     uint32_t i;      // matrix row            (i, chunk adjacent: one LDS.64)
@@ -159,8 +162,11 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         // ---- A: sojourn of every walker in flight
         bool fin = false, jmp = false;
         if (act) sojourn(fin, jmp);
-        const unsigned idle = __ballot_sync(FULL, !act);
-        if (idle) {  // scheduler work only when a lane is free
+        unsigned idle = __ballot_sync(FULL, !act);
+        // scheduler work only when enough lanes are free (batching pops
+        // amortises the scheduler over several walkers)
+        if (__popc(idle) < ENTRY_POP_MIN && idle != FULL) idle = 0;
+        if (idle) {
             // ---- admit: sweep chunks while queued tickets cannot feed the
             // idle lanes and a whole chunk's tickets fit in the ring
             while (live < R && atask < ntask && tail - head < (uint32_t)__popc(idle) &&
