@@ -75,6 +75,48 @@ float fm_neg_ln_u(uint32_t w) {
     return -ln_u;
 }
 
+/* exp_det of csrc/common.cuh: the kernel's deterministic fp64 exp. */
+double fm_exp(double x) {
+    if (!(x < 709.782712893384)) return x != x ? x : INFINITY;
+    if (x < -745.1332191019412) return 0.0;
+    const double n = rint(x * 1.4426950408889634);
+    double r = fma(-n, 6.93147180369123816490e-01, x);
+    r = fma(-n, 1.90821492927058770002e-10, r);
+    double q = 1.6059043836821614599e-10;
+    q = fma(q, r, 2.0876756987868098979e-09);
+    q = fma(q, r, 2.5052108385441718775e-08);
+    q = fma(q, r, 2.7557319223985890653e-07);
+    q = fma(q, r, 2.7557319223985890653e-06);
+    q = fma(q, r, 2.4801587301587301566e-05);
+    q = fma(q, r, 1.9841269841269841253e-04);
+    q = fma(q, r, 1.3888888888888889419e-03);
+    q = fma(q, r, 8.3333333333333332177e-03);
+    q = fma(q, r, 4.1666666666666664354e-02);
+    q = fma(q, r, 1.6666666666666665741e-01);
+    q = fma(q, r, 0.5);
+    q = fma(q, r, 1.0);
+    q = fma(q, r, 1.0);
+    const long long k = (long long)n;
+    uint64_t b;
+    double s;
+    if (k > 1023) {
+        b = (uint64_t)2046 << 52;
+        memcpy(&s, &b, 8);
+        return (q * 2.0) * s;
+    }
+    if (k >= -1022) {
+        b = (uint64_t)(k + 1023) << 52;
+        memcpy(&s, &b, 8);
+        return q * s;
+    }
+    b = (uint64_t)(k + 1023 + 54) << 52;
+    memcpy(&s, &b, 8);
+    double t;
+    uint64_t b2 = (uint64_t)(1023 - 54) << 52;
+    memcpy(&t, &b2, 8);
+    return (q * s) * t;
+}
+
 static uint32_t fm_pick(uint32_t hi, uint32_t lo, uint32_t n) {
     const uint64_t x = ((uint64_t)hi << 32) | lo;
     return (uint32_t)(((unsigned __int128)x * n) >> 64);
@@ -124,7 +166,7 @@ static double fm_walker(const fm_rec* rec, const uint32_t* nbr, const uint32_t* 
             const double Sp = strang ? S - 0.5 * cur.d : S;
             const double x = dt * (Sp - corr_i);
             *jumps += jc;
-            return exp(x) * cur.v - f0;
+            return fm_exp(x) * cur.v - f0;
         }
         const uint32_t kk = (uint32_t)ceil(tn);
         S = fma(cur.d, (double)(kk - g), S);
@@ -160,9 +202,9 @@ void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
     for (uint64_t r = 0; r < nrows; ++r) {
         const uint32_t i = rows[r];
         const fm_rec ri = rec[i];
-        const double p0 = exp(-(rate[i] * beta));
+        const double p0 = fm_exp(-(rate[i] * beta));
         const uint64_t T0 = (uint64_t)(p0 * 4294967296.0);
-        const double f0 = exp(beta * ri.d) * ri.v;
+        const double f0 = fm_exp(beta * ri.d) * ri.v;
         const double corr_i = strang ? 0.5 * ri.d : ri.d;
         double w1 = 0.0, w2 = 0.0;
         uint64_t wj = 0;

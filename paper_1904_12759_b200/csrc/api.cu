@@ -142,7 +142,7 @@ struct expmc_matrix {
     DevSplit m;
     std::vector<void*> owned;
     DevBuf vdev, rows, out_val, out_se, out_j, fa, vcum, values, pa, pb, pc, scal, tmp1, tmp2,
-        tmp3, iota, part;
+        tmp3, iota, part, fa2, sort_tmp;
     uint64_t iota_n = 0;
     // host copies kept for K5 norm bounds
     std::vector<double> h_rate, h_diag;
@@ -157,7 +157,7 @@ struct expmc_matrix {
     ~expmc_matrix() {
         for (void* p : owned) cudaFree(p);
         for (DevBuf* b : {&vdev, &rows, &out_val, &out_se, &out_j, &fa, &vcum, &values, &pa,
-                          &pb, &pc, &scal, &tmp1, &tmp2, &tmp3, &iota, &part})
+                          &pb, &pc, &scal, &tmp1, &tmp2, &tmp3, &iota, &part, &fa2, &sort_tmp})
             b->release();
         if (stream) cudaStreamDestroy(stream);
         if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -427,35 +427,77 @@ void run_scatter(expmc_matrix* h, int start_mode, const std::vector<double>* cum
     double* pa = h->pa.get<double>(parts);
     double* pb = h->pb.get<double>(parts);
     unsigned long long* pc = h->pc.get<unsigned long long>(parts);
-    if (p->rng == EXPMC_RNG_PHILOX) {
-        launch_scatter_fast(h->m, start_mode, vc, v_sum, fast_params(p, p->samples), vals, pa,
-                            pb, pc, s);
-    } else {
-        const double dt = p->beta / (double)p->n_steps;
-        const bool strang = p->splitting == EXPMC_STRANG;
-        double* f = h->fa.get<double>(n);
-        launch_node_factors(n, h->m.d, strang ? dt / 2.0 : dt, f, s);
+    const double dt = p->beta / (double)p->n_steps;
+    const bool strang = p->splitting == EXPMC_STRANG;
+    double* fac = nullptr;
+    if (p->rng != EXPMC_RNG_PHILOX) {
+        fac = h->fa.get<double>(n);
+        launch_node_factors(n, h->m.d, strang ? dt / 2.0 : dt, fac, s);
         after_launch(1);
-        // Lie weight on the state each segment leaves from (estimator.cpp:228-231)
-        launch_scatter_compat(h->m, start_mode, vc, v_sum, dt, p->n_steps, p->samples, f,
-                              strang ? f : nullptr, p->seed, vals, pa, pb, pc, s);
     }
-    after_launch(1);
-    double* tot = h->scal.get<double>(4);
-    launch_final_reduce(pa, pb, pc, parts, tot, tot + 1,
-                        reinterpret_cast<unsigned long long*>(tot + 2), s);
-    after_launch(1);
+    // walkers in batches; per batch: (end, f) records -> stable sort by end
+    // -> reduce-by-key -> values[] += run sums (deterministic, no atomics);
+    // scalar tallies reduced per batch and added on the host in batch order
+    const uint64_t M = p->samples;
+    const uint64_t B = vals ? std::min<uint64_t>(M, 1ull << 25) : M;
+    uint32_t *rec_end = nullptr, *end_sorted = nullptr, *run_keys = nullptr;
+    double *rec_f = nullptr, *f_sorted = nullptr, *run_sums = nullptr;
+    int* nruns = nullptr;
+    void* temp = nullptr;
+    size_t temp_bytes = 0;
     if (vals) {
-        launch_scale(n, vals, 1.0 / (double)p->samples, s);
+        rec_end = h->tmp1.get<uint32_t>(B * 2);
+        end_sorted = rec_end + B;
+        rec_f = h->tmp2.get<double>(B * 2);
+        f_sorted = rec_f + B;
+        run_keys = h->tmp3.get<uint32_t>(B + 2);
+        run_sums = h->fa2.get<double>(B);
+        nruns = reinterpret_cast<int*>(run_keys + B);
+        temp_bytes = scatter_sort_temp_bytes(B, n);
+        temp = h->sort_tmp.get<unsigned char>(temp_bytes);
+    }
+    const FastParams fp = fast_params(p, M);
+    double* tot = h->scal.get<double>(4);
+    double sum = 0.0, sq = 0.0;
+    uint64_t jumps = 0;
+    for (uint64_t l0 = 0; l0 < M; l0 += B) {
+        const uint64_t lend = std::min(M, l0 + B);
+        if (p->rng == EXPMC_RNG_PHILOX) {
+            launch_scatter_fast(h->m, start_mode, vc, v_sum, fp, l0, lend, rec_end, rec_f, pa, pb,
+                                pc, s);
+        } else {
+            // Lie weight on the state each segment leaves from (estimator.cpp:228-231)
+            launch_scatter_compat(h->m, start_mode, vc, v_sum, dt, p->n_steps, M, fac,
+                                  strang ? fac : nullptr, p->seed, l0, lend, rec_end, rec_f, pa,
+                                  pb, pc, s);
+        }
+        launch_final_reduce(pa, pb, pc, parts, tot, tot + 1,
+                            reinterpret_cast<unsigned long long*>(tot + 2), s);
+        after_launch(2);
+        if (vals) {
+            scatter_sort_accumulate(rec_end, rec_f, end_sorted, f_sorted, lend - l0, n, run_keys,
+                                    run_sums, nruns, temp, temp_bytes, vals, s);
+            after_launch(1);
+            CK(cudaGetLastError());
+        }
+        double res[3];
+        CK(cudaMemcpyAsync(res, tot, sizeof(res), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        uint64_t j;
+        std::memcpy(&j, &res[2], 8);
+        sum += res[0];
+        sq += res[1];
+        jumps += j;
+    }
+    if (vals) {
+        launch_scale(n, vals, 1.0 / (double)M, s);
         after_launch(1);
         CK(cudaMemcpyAsync(values_host, vals, n * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
     }
-    double res[3];
-    CK(cudaMemcpyAsync(res, tot, sizeof(res), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    *sum_out = res[0];
-    *sq_out = res[1];
-    std::memcpy(jumps_out, &res[2], 8);
+    *sum_out = sum;
+    *sq_out = sq;
+    *jumps_out = jumps;
 }
 
 void finalize(double sum, double sum_sq, uint64_t ms, double* value, double* se) {

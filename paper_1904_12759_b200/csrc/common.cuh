@@ -161,6 +161,39 @@ __device__ __forceinline__ float neg_ln_u(uint32_t w) {
     return -ln_u;
 }
 
+// e^x in fp64 from IEEE-exact operations only (rint, fma, mul), so the CPU
+// model (oracle/fast_model.c fm_exp) reproduces it bit for bit: Cody-Waite
+// reduction x = n ln2 + r, |r| <= ln2/2, degree-13 Taylor for e^r, exact
+// scaling by 2^n.  Max error ~1 ulp on [-745, 709.78].
+__device__ __forceinline__ double exp_det(double x) {
+    if (!(x < 709.782712893384)) return x != x ? x : __longlong_as_double(0x7ff0000000000000LL);
+    if (x < -745.1332191019412) return 0.0;
+    const double n = rint(__dmul_rn(x, 1.4426950408889634));
+    double r = __fma_rn(-n, 6.93147180369123816490e-01, x);
+    r = __fma_rn(-n, 1.90821492927058770002e-10, r);
+    double q = 1.6059043836821614599e-10;  // 1/13!
+    q = __fma_rn(q, r, 2.0876756987868098979e-09);
+    q = __fma_rn(q, r, 2.5052108385441718775e-08);
+    q = __fma_rn(q, r, 2.7557319223985890653e-07);
+    q = __fma_rn(q, r, 2.7557319223985890653e-06);
+    q = __fma_rn(q, r, 2.4801587301587301566e-05);
+    q = __fma_rn(q, r, 1.9841269841269841253e-04);
+    q = __fma_rn(q, r, 1.3888888888888889419e-03);
+    q = __fma_rn(q, r, 8.3333333333333332177e-03);
+    q = __fma_rn(q, r, 4.1666666666666664354e-02);
+    q = __fma_rn(q, r, 1.6666666666666665741e-01);
+    q = __fma_rn(q, r, 0.5);
+    q = __fma_rn(q, r, 1.0);
+    q = __fma_rn(q, r, 1.0);
+    const long long k = (long long)n;
+    if (k > 1023)  // 2^1024 is not representable: q * 2 * 2^1023
+        return __dmul_rn(__dmul_rn(q, 2.0), __longlong_as_double(2046LL << 52));
+    if (k >= -1022)
+        return __dmul_rn(q, __longlong_as_double((k + 1023) << 52));
+    return __dmul_rn(__dmul_rn(q, __longlong_as_double((k + 1023 + 54) << 52)),
+                     __longlong_as_double((long long)(1023 - 54) << 52));
+}
+
 // floor(x * n / 2^64) for a 64-bit uniform x: unbiased to n / 2^64.
 __device__ __forceinline__ uint32_t pick_index(uint32_t hi, uint32_t lo,
                                                uint32_t n) {

@@ -73,8 +73,16 @@ void launch_entry_compat(const DevSplit& m, const double* v, const uint32_t* row
 unsigned scatter_compat_grid();
 void launch_scatter_compat(const DevSplit& m, int start_mode, const double* vcum, double v_sum,
                            double dt, uint64_t n_steps, uint64_t samples, const double* before,
-                           const double* after, uint64_t seed, double* values, double* part_sum,
-                           double* part_sq, unsigned long long* part_j, cudaStream_t s);
+                           const double* after, uint64_t seed, uint64_t l0, uint64_t lend,
+                           uint32_t* out_end, double* out_f, double* part_sum, double* part_sq,
+                           unsigned long long* part_j, cudaStream_t s);
+
+// scatter_sort.cu
+size_t scatter_sort_temp_bytes(uint64_t batch, uint64_t n);
+void scatter_sort_accumulate(uint32_t* end, double* f, uint32_t* end_sorted, double* f_sorted,
+                             uint64_t count, uint64_t n, uint32_t* run_keys, double* run_sums,
+                             int* nruns, void* temp, size_t temp_bytes, double* values,
+                             cudaStream_t s);
 
 // walk_fast.cu (K3, K4, K6)
 int entry_fast_wpr(uint64_t W);
@@ -85,7 +93,8 @@ int launch_entry_fast(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
                       void* scratch, cudaStream_t s);
 unsigned scatter_fast_grid();
 void launch_scatter_fast(const DevSplit& m, int start_mode, const double* vcum, double v_sum,
-                         const FastParams& p, double* values, double* part_s1, double* part_s2,
+                         const FastParams& p, uint64_t l0, uint64_t lend, uint32_t* out_end,
+                         double* out_f, double* part_s1, double* part_s2,
                          unsigned long long* part_j, cudaStream_t s);
 void launch_gather_ceiling(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
                            uint32_t chains_per_row, uint32_t chain_len, uint32_t salt,

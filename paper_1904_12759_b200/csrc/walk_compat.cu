@@ -141,14 +141,15 @@ __global__ void __launch_bounds__(kCompatBS)
 scatter_compat_kernel(SoA m, uint64_t n, int start_mode, const double* __restrict__ vcum,
                       double v_sum, double dt, uint64_t n_steps, uint64_t samples,
                       const double* __restrict__ before, const double* __restrict__ after,
-                      uint64_t seed, double* __restrict__ values, double* __restrict__ part_sum,
+                      uint64_t seed, uint64_t l0, uint64_t lend, uint32_t* __restrict__ out_end,
+                      double* __restrict__ out_f, double* __restrict__ part_sum,
                       double* __restrict__ part_sq, unsigned long long* __restrict__ part_j) {
     __shared__ double sa[kCompatBS], sb[kCompatBS];
     __shared__ unsigned long long sc[kCompatBS];
     double sum = 0.0, sum_sq = 0.0;
     unsigned long long jumps = 0;
     const uint64_t stride = (uint64_t)gridDim.x * kCompatBS;
-    for (uint64_t l = blockIdx.x * (uint64_t)kCompatBS + threadIdx.x; l < samples; l += stride) {
+    for (uint64_t l = l0 + blockIdx.x * (uint64_t)kCompatBS + threadIdx.x; l < lend; l += stride) {
         Pcg32 rng(seed, l);
         uint32_t start;
         if (start_mode == 0) {
@@ -170,7 +171,10 @@ scatter_compat_kernel(SoA m, uint64_t n, int start_mode, const double* __restric
         sum = __dadd_rn(sum, f);
         sum_sq = __dadd_rn(sum_sq, __dmul_rn(f, f));
         jumps += j;
-        if (values) atomicAdd(values + end, f);
+        if (out_end) {  // (end, f) record for the deterministic per-end reduction
+            out_end[l - l0] = end;
+            out_f[l - l0] = f;
+        }
     }
     block_sum3<kCompatBS>(sum, sum_sq, jumps, sa, sb, sc);
     if (threadIdx.x == 0) {
@@ -198,12 +202,13 @@ unsigned scatter_compat_grid() { return 148 * 8; }
 
 void launch_scatter_compat(const DevSplit& m, int start_mode, const double* vcum, double v_sum,
                            double dt, uint64_t n_steps, uint64_t samples, const double* before,
-                           const double* after, uint64_t seed, double* values, double* part_sum,
-                           double* part_sq, unsigned long long* part_j, cudaStream_t s) {
+                           const double* after, uint64_t seed, uint64_t l0, uint64_t lend,
+                           uint32_t* out_end, double* out_f, double* part_sum, double* part_sq,
+                           unsigned long long* part_j, cudaStream_t s) {
     SoA a{m.rate, m.row_offset, m.neighbor, m.cum, m.uniform_row};
     scatter_compat_kernel<<<scatter_compat_grid(), kCompatBS, 0, s>>>(
-        a, m.n, start_mode, vcum, v_sum, dt, n_steps, samples, before, after, seed, values,
-        part_sum, part_sq, part_j);
+        a, m.n, start_mode, vcum, v_sum, dt, n_steps, samples, before, after, seed, l0, lend,
+        out_end, out_f, part_sum, part_sq, part_j);
 }
 
 }  // namespace expmc_b200

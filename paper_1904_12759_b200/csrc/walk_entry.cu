@@ -112,11 +112,11 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             RowConst& a = q.adm;
             const uint32_t i = rows[t / WPR];
             const RowRec ri = load_rec(rec, i);
-            const double p0 = exp(-__dmul_rn(__ldg(rate + i), p.beta));
+            const double p0 = exp_det(-__dmul_rn(__ldg(rate + i), p.beta));
             a.rr = ri;
             a.i = i;
             a.T0 = (unsigned long long)__dmul_rn(p0, 4294967296.0);
-            a.f0 = __dmul_rn(exp(__dmul_rn(p.beta, ri.d)), ri.v);
+            a.f0 = __dmul_rn(exp_det(__dmul_rn(p.beta, ri.d)), ri.v);
             a.corr = p.strang ? __dmul_rn(0.5, ri.d) : ri.d;
         }
         __syncwarp();
@@ -260,7 +260,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             for (uint32_t k = ts + lane; k < te; k += 32) {
                 const uint32_t pos = k & (CAP - 1);
                 const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], corr));
-                q.dev[q.rs[pos] & 255u] = __dsub_rn(__dmul_rn(exp(x), q.v[pos]), f0);
+                q.dev[q.rs[pos] & 255u] = __dsub_rn(__dmul_rn(exp_det(x), q.v[pos]), f0);
                 jl += q.w[pos];
             }
             __syncwarp();

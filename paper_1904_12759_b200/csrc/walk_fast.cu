@@ -20,12 +20,13 @@ namespace {
 __global__ void __launch_bounds__(128)
 scatter_fast_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj,
                     const uint32_t* __restrict__ thr, const uint32_t* __restrict__ alias, uint64_t n, int start_mode, const double* __restrict__ vcum, double v_sum,
-                    FastParams p, double* __restrict__ values, double* __restrict__ part_s1,
+                    FastParams p, uint64_t l0, uint64_t lend, uint32_t* __restrict__ out_end,
+                    double* __restrict__ out_f, double* __restrict__ part_s1,
                     double* __restrict__ part_s2, unsigned long long* __restrict__ part_j) {
     __shared__ double sh1[4], sh2[4];
     __shared__ unsigned long long shj[4];
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    uint64_t l = l0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     double s1 = 0.0, s2 = 0.0;
     unsigned long long jt = 0;
     bool active = false;
@@ -34,7 +35,7 @@ scatter_fast_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj
     double dcur = 0.0, t = 0.0, S = 0.0, corr0 = 0.0;
     while (true) {
         if (!active) {
-            if (l >= p.W) break;
+            if (l >= lend) break;
             const U4 ws = philox4x32_10(U4{0xffffffffu, (uint32_t)l, (uint32_t)(l >> 32),
                                            kTagScatter}, p.rk);
             uint32_t s;
@@ -70,7 +71,10 @@ scatter_fast_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj
             s1 = __dadd_rn(s1, f);
             s2 = __fma_rn(f, f, s2);
             jt += jc;
-            if (values) atomicAdd(values + cur, f);
+            if (out_end) {  // (end, f) record for the deterministic per-end reduction
+                out_end[l - l0] = cur;
+                out_f[l - l0] = f;
+            }
             active = false;
             l += stride;
         } else {
@@ -141,11 +145,12 @@ gather_ceiling_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ a
 unsigned scatter_fast_grid() { return 148 * 12; }
 
 void launch_scatter_fast(const DevSplit& m, int start_mode, const double* vcum, double v_sum,
-                         const FastParams& p, double* values, double* part_s1, double* part_s2,
+                         const FastParams& p, uint64_t l0, uint64_t lend, uint32_t* out_end,
+                         double* out_f, double* part_s1, double* part_s2,
                          unsigned long long* part_j, cudaStream_t s) {
     scatter_fast_kernel<<<scatter_fast_grid(), 128, 0, s>>>(
-        m.rec, m.adj, m.alias_thr, m.alias_idx, m.n, start_mode, vcum, v_sum, p, values,
-        part_s1, part_s2, part_j);
+        m.rec, m.adj, m.alias_thr, m.alias_idx, m.n, start_mode, vcum, v_sum, p, l0, lend,
+        out_end, out_f, part_s1, part_s2, part_j);
 }
 
 void launch_gather_ceiling(const DevSplit& m, const uint32_t* rows, uint64_t nrows,

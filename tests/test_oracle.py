@@ -157,6 +157,23 @@ def test_model_neg_ln_accuracy(orc):
         assert abs(got - want) <= 2e-7 * max(1.0, want), (w, got, want)
 
 
+def test_model_exp_det_accuracy(orc):
+    """The walker's deterministic exp (exp_det / fm_exp) is within 1 ulp of
+    glibc exp over the whole finite range, including subnormal results."""
+    import ctypes
+
+    f = orc.L.fm_exp
+    f.restype = ctypes.c_double
+    f.argtypes = [ctypes.c_double]
+    rng = np.random.default_rng(0)
+    xs = np.concatenate([rng.uniform(-745, 709.78, 20000), rng.uniform(-3, 3, 20000),
+                         [0.0, 709.43, 709.44, 709.78, -708.4, -744.9]])
+    for x in xs:
+        a, b = f(float(x)), math.exp(float(x))
+        assert abs(a - b) <= math.ulp(b), (x, a, b)
+    assert math.isinf(f(710.0)) and f(-800.0) == 0.0
+
+
 def test_model_law_matches_reference(orc, ref):
     """The continuous-clock Philox walker (CPU model of K3) samples the same
     law as the reference: per-entry z-scores over several graphs."""
