@@ -74,6 +74,14 @@ int expmc_cuda_abi_version(void); /* 1 */
 int expmc_cuda_create_from_csr(uint64_t n, const uint64_t* row_ptr, const uint32_t* col,
                                const double* val, const double* diag, int device,
                                expmc_matrix** out);
+/* From a raw entry list, exactly SparseSymmetric::from_entries
+ * (sparse_matrix.cpp:18-85) on the device: entries may come in either
+ * triangle and any order; validated with the reference's messages and
+ * precedence (first offending entry in input order, then the first duplicate
+ * after canonical sorting), sorted, mirrored, then split on the device. */
+int expmc_cuda_create_from_entries(uint64_t n, const uint32_t* rows, const uint32_t* cols,
+                                   const double* weights, uint64_t n_entries, int device,
+                                   expmc_matrix** out);
 /* From an existing reference SplitMatrix (sparse_matrix.hpp:66-91): its
  * row_offset / neighbor / weight / diag fields.  rate, cum, d, uniform_row,
  * dbar and dmax are re-derived on the device bit-exactly. */

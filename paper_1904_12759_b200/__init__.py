@@ -8,7 +8,7 @@ The reference's estimator API (arXiv 1904.12759 C++ artifact,
 from ._lib import ExpmcError, lib
 from .estimator import (EntriesEstimate, Estimate, PathParams, Rng, SplitMatrix, Splitting,
                         VectorEstimate, entries_device, entries_estimate, entry_estimate,
-                        entry_slots, expmv, gather_ceiling_device, launch_count, set_v_device,
+                        entry_slots, expmv, from_entries, gather_ceiling_device, launch_count, set_v_device,
                         split, splitting_product, tc_estimate, vector_estimate)
 from .inputs import Csr, build_config, csr_from_dense, gen_ba, gen_fd, gen_row_sample, gen_vector, gen_ws, n_rule
 from .spectral import BetaRule, lambda_max, resolve_beta

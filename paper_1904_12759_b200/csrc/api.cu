@@ -189,6 +189,59 @@ const uint32_t* all_rows(expmc_matrix* h) {
     return d;
 }
 
+void alloc_split(expmc_matrix* h, uint64_t n, uint64_t nnz) {
+    DevSplit& m = h->m;
+    m.n = n;
+    m.nnz = nnz;
+    m.diag = h->alloc<double>(n);
+    m.d = h->alloc<double>(n);
+    m.rate = h->alloc<double>(n);
+    m.row_offset = h->alloc<uint64_t>(n + 1);
+    m.neighbor = h->alloc<uint32_t>(nnz);
+    m.weight = h->alloc<double>(nnz);
+    m.cum = h->alloc<double>(nnz);
+    m.uniform_row = h->alloc<uint8_t>(n);
+    m.rec = h->alloc<RowRec>(n);
+}
+
+// K1 on an uploaded (valid) mirrored CSR: split(), alias tables, fat
+// adjacency (sparse_matrix.cpp:101-142 + the B200 walk layout).
+void finish_split(expmc_matrix* h) {
+    DevSplit& m = h->m;
+    const uint64_t n = m.n, nnz = m.nnz;
+    cudaStream_t s = h->stream;
+    unsigned long long* sc = h->scal.get<unsigned long long>(4);
+    const unsigned long long init[4] = {~0ull, 0ull, 0ull, 0ull};
+    CK(cudaMemcpyAsync(sc, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    launch_split_pack(n, m.row_offset, m.weight, m.diag, m.d, m.rate, m.cum, m.uniform_row, m.rec,
+                      sc + 1, reinterpret_cast<unsigned int*>(sc + 2), s);
+    after_launch(n ? 1 : 0);
+    unsigned long long res[4];
+    CK(cudaMemcpyAsync(res, sc, sizeof(res), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    m.dmax = res[1];
+    m.any_nonuniform = (res[2] & 0xffffffffull) != 0;
+    m.dbar = n > 0 ? (double)nnz / (double)n : 0.0;  // sparse_matrix.cpp:138-141
+    if (m.any_nonuniform) {
+        m.alias_thr = h->alloc<uint32_t>(nnz);
+        m.alias_idx = h->alloc<uint32_t>(nnz);
+        double* p = h->tmp1.get<double>(nnz);
+        uint32_t* sm = h->tmp2.get<uint32_t>(nnz);
+        uint32_t* lg = h->tmp3.get<uint32_t>(nnz);
+        launch_alias_build(n, m.row_offset, m.weight, m.rate, m.uniform_row, m.alias_thr,
+                           m.alias_idx, p, sm, lg, s);
+        after_launch(1);
+        CK(cudaStreamSynchronize(s));
+        h->tmp1.release();
+        h->tmp2.release();
+        h->tmp3.release();
+    }
+    m.adj = h->alloc<Edge>(nnz);
+    launch_build_adj(nnz, m.neighbor, m.rec, m.adj, s);
+    after_launch(nnz ? 1 : 0);
+    CK(cudaStreamSynchronize(s));
+}
+
 expmc_matrix* build(uint64_t n, const uint64_t* row_ptr, const uint32_t* col, const double* val,
                     const double* diag, int device) {
     if (n >= (1ull << 32)) throw InvalidArg("n must be < 2^32 (NodeId is 32-bit)");
@@ -211,18 +264,8 @@ expmc_matrix* build(uint64_t n, const uint64_t* row_ptr, const uint32_t* col, co
         CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&h->piece_done, cudaEventDisableTiming));
+        alloc_split(h, n, nnz);
         DevSplit& m = h->m;
-        m.n = n;
-        m.nnz = nnz;
-        m.diag = h->alloc<double>(n);
-        m.d = h->alloc<double>(n);
-        m.rate = h->alloc<double>(n);
-        m.row_offset = h->alloc<uint64_t>(n + 1);
-        m.neighbor = h->alloc<uint32_t>(nnz);
-        m.weight = h->alloc<double>(nnz);
-        m.cum = h->alloc<double>(nnz);
-        m.uniform_row = h->alloc<uint8_t>(n);
-        m.rec = h->alloc<RowRec>(n);
         cudaStream_t s = h->stream;
         if (n) {
             CK(cudaMemcpyAsync(m.row_offset, row_ptr, (n + 1) * 8, cudaMemcpyHostToDevice, s));
@@ -269,33 +312,36 @@ expmc_matrix* build(uint64_t n, const uint64_t* row_ptr, const uint32_t* col, co
                     throw InvalidArg("matrix is not symmetric at " + pair_str(i, j));
             }
         }
-        launch_split_pack(n, m.row_offset, m.weight, m.diag, m.d, m.rate, m.cum,
-                          m.uniform_row, m.rec, sc + 1, reinterpret_cast<unsigned int*>(sc + 2),
-                          s);
-        after_launch(n ? 1 : 0);
-        CK(cudaMemcpyAsync(res, sc, sizeof(res), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        m.dmax = res[1];
-        m.any_nonuniform = (res[2] & 0xffffffffull) != 0;
-        m.dbar = n > 0 ? (double)nnz / (double)n : 0.0;  // sparse_matrix.cpp:138-141
-        if (m.any_nonuniform) {
-            m.alias_thr = h->alloc<uint32_t>(nnz);
-            m.alias_idx = h->alloc<uint32_t>(nnz);
-            double* p = h->tmp1.get<double>(nnz);
-            uint32_t* sm = h->tmp2.get<uint32_t>(nnz);
-            uint32_t* lg = h->tmp3.get<uint32_t>(nnz);
-            launch_alias_build(n, m.row_offset, m.weight, m.rate, m.uniform_row, m.alias_thr,
-                               m.alias_idx, p, sm, lg, s);
-            after_launch(1);
-            CK(cudaStreamSynchronize(s));
-            h->tmp1.release();
-            h->tmp2.release();
-            h->tmp3.release();
+        finish_split(h);
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    return h;
+}
+
+// Device-side CSR (from_entries_device output, valid by construction).
+expmc_matrix* build_device_csr(uint64_t n, uint64_t nnz, const uint64_t* row_ptr_d,
+                               const uint32_t* col_d, const double* val_d, const double* diag_d,
+                               int device) {
+    DeviceGuard g(device);
+    auto* h = new expmc_matrix;
+    try {
+        h->device = device;
+        CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h->piece_done, cudaEventDisableTiming));
+        alloc_split(h, n, nnz);
+        DevSplit& m = h->m;
+        cudaStream_t s = h->stream;
+        CK(cudaMemcpyAsync(m.row_offset, row_ptr_d, (n + 1) * 8, cudaMemcpyDeviceToDevice, s));
+        if (n) CK(cudaMemcpyAsync(m.diag, diag_d, n * 8, cudaMemcpyDeviceToDevice, s));
+        if (nnz) {
+            CK(cudaMemcpyAsync(m.neighbor, col_d, nnz * 4, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(m.weight, val_d, nnz * 8, cudaMemcpyDeviceToDevice, s));
         }
-        m.adj = h->alloc<Edge>(nnz);
-        launch_build_adj(nnz, m.neighbor, m.rec, m.adj, s);
-        after_launch(nnz ? 1 : 0);
-        CK(cudaStreamSynchronize(s));
+        h->scal.get<unsigned long long>(4);
+        finish_split(h);
     } catch (...) {
         delete h;
         throw;
@@ -587,6 +633,70 @@ int expmc_cuda_create_from_csr(uint64_t n, const uint64_t* row_ptr, const uint32
     return guarded([&] {
         if (!out) throw InvalidArg("out is null");
         *out = build(n, row_ptr, col, val, diag, device);
+    });
+}
+
+int expmc_cuda_create_from_entries(uint64_t n, const uint32_t* rows, const uint32_t* cols,
+                                   const double* w, uint64_t ne, int device, expmc_matrix** out) {
+    // SparseSymmetric::from_entries (sparse_matrix.cpp:18-85) on the device
+    return guarded([&] {
+        if (!out) throw InvalidArg("out is null");
+        if (n >= (1ull << 32)) throw InvalidArg("n must be < 2^32 (NodeId is 32-bit)");
+        if (ne >= (1ull << 30)) throw InvalidArg("at most 2^30 entries");
+        if (ne && (!rows || !cols || !w)) throw InvalidArg("entry arrays are null");
+        DeviceGuard g(device);
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        uint32_t *r_d = nullptr, *c_d = nullptr, *col = nullptr;
+        double *w_d = nullptr, *diag_d = nullptr, *val = nullptr;
+        uint64_t* rp_d = nullptr;
+        auto cleanup = [&] {
+            cudaFree(r_d); cudaFree(c_d); cudaFree(w_d); cudaFree(diag_d); cudaFree(rp_d);
+            cudaFree(col); cudaFree(val);
+            cudaStreamDestroy(s);
+        };
+        try {
+            CK(cudaMalloc(&r_d, (ne ? ne : 1) * 4));
+            CK(cudaMalloc(&c_d, (ne ? ne : 1) * 4));
+            CK(cudaMalloc(&w_d, (ne ? ne : 1) * 8));
+            CK(cudaMalloc(&diag_d, (n ? n : 1) * 8));
+            CK(cudaMalloc(&rp_d, (n + 1) * 8));
+            if (ne) {
+                CK(cudaMemcpyAsync(r_d, rows, ne * 4, cudaMemcpyHostToDevice, s));
+                CK(cudaMemcpyAsync(c_d, cols, ne * 4, cudaMemcpyHostToDevice, s));
+                CK(cudaMemcpyAsync(w_d, w, ne * 8, cudaMemcpyHostToDevice, s));
+            }
+            uint64_t nnz = 0;
+            unsigned long long err[2] = {~0ull, ~0ull}, dup = 0;
+            from_entries_device(n, r_d, c_d, w_d, ne, rp_d, &col, &val, diag_d, &nnz, err, &dup,
+                                s);
+            CK(cudaGetLastError());
+            auto raw = [&](uint64_t k) {  // entry_str of the input entry
+                return "(" + std::to_string(rows[k]) + ", " + std::to_string(cols[k]) + ")";
+            };
+            if (err[0] != ~0ull) {
+                const uint64_t k = err[0] >> 3;
+                switch ((int)(err[0] & 7)) {
+                    case 1:
+                        throw InvalidArg("entry " + raw(k) + " out of range for n = " +
+                                         std::to_string(n));
+                    case 2: throw InvalidArg("non-finite weight at " + raw(k));
+                    case 3: throw InvalidArg("explicit zero entry at " + raw(k));
+                    default:
+                        throw InvalidArg("negative off-diagonal weight at " + raw(k) +
+                                         ": no CTMC interpretation");
+                }
+            }
+            if (err[1] != ~0ull)
+                throw InvalidArg("duplicate entry at (" + std::to_string(dup >> 32) + ", " +
+                                 std::to_string(dup & 0xffffffffull) + ")");
+            if (nnz >= (1ull << 32)) throw InvalidArg("nnz must be < 2^32");
+            *out = build_device_csr(n, nnz, rp_d, col, val, diag_d, device);
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
     });
 }
 

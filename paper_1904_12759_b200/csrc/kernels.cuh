@@ -77,6 +77,12 @@ void launch_scatter_compat(const DevSplit& m, int start_mode, const double* vcum
                            uint32_t* out_end, double* out_f, double* part_sum, double* part_sq,
                            unsigned long long* part_j, cudaStream_t s);
 
+// from_entries.cu (§8f f1)
+void from_entries_device(uint64_t n, const uint32_t* r, const uint32_t* c, const double* w,
+                         uint64_t ne, uint64_t* row_ptr, uint32_t** col_out, double** val_out,
+                         double* diag, uint64_t* nnz_out, unsigned long long* err_host,
+                         unsigned long long* dup_key, cudaStream_t s);
+
 // scatter_sort.cu
 size_t scatter_sort_temp_bytes(uint64_t batch, uint64_t n);
 void scatter_sort_accumulate(uint32_t* end, double* f, uint32_t* end_sorted, double* f_sorted,

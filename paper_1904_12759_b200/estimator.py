@@ -197,6 +197,22 @@ class SplitMatrix:
         return out
 
 
+def from_entries(n: int, rows, cols, weights, device=0) -> SplitMatrix:
+    """SparseSymmetric::from_entries + split() (sparse_matrix.cpp:18-85,
+    :101-142) on the GPU: raw (row, col, weight) entries in either triangle
+    and any order; the reference's validation messages and precedence."""
+    r = np.ascontiguousarray(rows, dtype=np.uint32)
+    c = np.ascontiguousarray(cols, dtype=np.uint32)
+    w = _f64(weights)
+    if not (len(r) == len(c) == len(w)):
+        raise ValueError("rows, cols and weights must have the same length")
+    h = C.c_void_p()
+    check(lib().expmc_cuda_create_from_entries(int(n), r.ctypes.data_as(u32p),
+                                               c.ctypes.data_as(u32p), w.ctypes.data_as(f64p),
+                                               len(w), int(device), C.byref(h)))
+    return SplitMatrix(h, n)
+
+
 def split(csr, device=0) -> SplitMatrix:
     """split(SparseSymmetric) (sparse_matrix.cpp:101-142), on the GPU.
     ``csr`` has ``n, row_ptr, col, val, diag`` (see :class:`inputs.Csr`)."""

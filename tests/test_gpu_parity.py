@@ -355,6 +355,49 @@ def test_cpp_header_api_runs(tmp_path, pb):
     assert "api_demo ok" in r.stdout
 
 
+def test_from_entries_on_device_matches_reference(pb, ref):
+    """§8f f1: GPU from_entries + split is bit-exact with the reference's
+    SparseSymmetric::from_entries + split (shuffled, mixed triangles)."""
+    rng = np.random.default_rng(3)
+    for n, ne in ((1, 0), (7, 9), (500, 3000), (20000, 120000)):
+        pairs = set()
+        rows, cols, w = [], [], []
+        while len(rows) < ne:
+            i, j = (int(x) for x in rng.integers(0, n, 2))
+            key = (min(i, j), max(i, j))
+            if key in pairs:
+                continue
+            pairs.add(key)
+            rows.append(i)
+            cols.append(j)
+            w.append(float(rng.normal()) if i == j else float(rng.integers(1, 8)) / 2.0)
+        m = pb.from_entries(n, rows, cols, w)
+        rs = ref.matrix_from_entries(n, rows, cols, w).split()
+        dev = m.export()
+        for k in ("diag", "d", "rate", "cum", "uniform_row", "row_offset", "neighbor", "weight"):
+            assert np.array_equal(dev[k], rs[k]), (n, k)
+        assert m.dbar == rs["dbar"] and m.dmax == rs["dmax"]
+
+
+def test_from_entries_errors_match_reference(pb, ref):
+    import oracle
+
+    cases = [
+        (3, [0, 5, 1], [1, 0, 1], [1.0, 1.0, 1.0]),        # out of range
+        (3, [0, 1, 2], [1, 2, 2], [1.0, np.nan, 1.0]),     # non-finite
+        (3, [0, 1], [1, 1], [0.0, 1.0]),                   # explicit zero
+        (3, [2, 0], [1, 1], [-1.0, 1.0]),                  # negative off-diagonal
+        (3, [0, 1, 2], [1, 0, 2], [1.0, 1.0, 1.0]),        # mirrored duplicate
+        (3, [0, 2, 1], [5, 1, 1], [np.inf, -2.0, 0.0]),    # precedence: first in input order
+    ]
+    for n, r, c, w in cases:
+        with pytest.raises(oracle.RefError) as er:
+            ref.matrix_from_entries(n, r, c, w)
+        with pytest.raises(ValueError) as eg:
+            pb.from_entries(n, r, c, w)
+        assert str(eg.value) == str(er.value)
+
+
 @pytest.mark.parametrize("rng", [0, 1])
 def test_vector_estimate_is_bitwise_deterministic(pb, graphs, rng):
     """Per-end accumulation by sort + reduce-by-key (no atomics): repeated
