@@ -156,6 +156,15 @@ int expmc_cuda_lambda_max(expmc_matrix* m, uint64_t power_iters, double* lambda_
 int expmc_cuda_splitting_product(expmc_matrix* m, const double* v, uint64_t nv,
                                  const expmc_path_params* p, double tol, double* out);
 
+/* ------------------------------------------------ ranking metrics (f4) */
+/* rank() (metrics.cpp:10-25): order[] = node ids by descending score, ties
+ * by ascending id; "rank: NaN score" on NaN. */
+int expmc_cuda_rank(const double* scores, uint64_t n, int device, uint32_t* order);
+/* isim() (metrics.cpp:27-55) of two rankings' top ceil(top_fraction * n)
+ * prefixes; same checks and messages as the reference. */
+int expmc_cuda_isim(const uint32_t* order_x, const uint32_t* order_y, uint64_t nx, uint64_t ny,
+                    double top_fraction, int device, double* out);
+
 /* ----------------------------------------- synthetic inputs (host, C++) */
 /* Host CSR builders for the benchmark configurations.  The returned object
  * owns a mirrored, row-sorted CSR (the SparseSymmetric adjacency) plus the

@@ -226,6 +226,22 @@ class Ref:
         L.ref_exp_times.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_uint64, _f64p]
         L.ref_advance.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64,
                                   _u32p, _u64p]
+        L.ref_rank.argtypes = [_f64p, C.c_uint64, _u32p]
+        L.ref_isim.argtypes = [_u32p, _u32p, C.c_uint64, C.c_uint64, C.c_double, _f64p]
+
+    def rank(self, values):
+        v = np.ascontiguousarray(values, np.float64)
+        out = np.zeros(len(v), np.uint32)
+        self._chk(self.L.ref_rank(_p(v, _f64p), len(v), _p(out, _u32p)))
+        return out
+
+    def isim(self, ox, oy, top_fraction):
+        ox = np.ascontiguousarray(ox, np.uint32)
+        oy = np.ascontiguousarray(oy, np.uint32)
+        out = C.c_double()
+        self._chk(self.L.ref_isim(_p(ox, _u32p), _p(oy, _u32p), len(ox), len(oy), top_fraction,
+                                  C.byref(out)))
+        return out.value
 
     def _chk(self, rc):
         if rc != 0:

@@ -146,13 +146,15 @@ static double fm_walker(const fm_rec* rec, const uint32_t* nbr, const uint32_t* 
                         const uint32_t* alias, uint32_t i, uint64_t l, uint64_t T0,
                         double f0, double corr_i, double dt, double inv_dt, double n_grid,
                         uint64_t N, int strang, uint32_t k0, uint32_t k1,
-                        uint64_t* jumps) {
+                        uint64_t* jumps, int* jumped) {
     const uint32_t base = (uint32_t)((l / 128) * 128);
     const uint32_t dctr[4] = {0xffffffffu, base + (uint32_t)(l % 32), i, FM_TAG_ENTRY};
     uint32_t dw[4];
     fm_philox(dctr, k0, k1, dw);
     const uint32_t ew0 = dw[(l % 128) / 32];
-    if ((uint64_t)ew0 < T0) return 0.0; /* never jumps */
+    *jumped = 0;
+    if ((uint64_t)ew0 < T0) return 0.0; /* never jumps: accounted per part */
+    *jumped = 1;
     fm_rec cur = rec[i];
     uint32_t ew = ew0, g = 0, jc = 0;
     double t = 0.0, S = 0.0;
@@ -205,6 +207,8 @@ void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
         const double p0 = fm_exp(-(rate[i] * beta));
         const uint64_t T0 = (uint64_t)(p0 * 4294967296.0);
         const double f0 = fm_exp(beta * ri.d) * ri.v;
+        /* deviation shift: f0 if never-jumpers are the majority, else 0 */
+        const double K = T0 >= (1ull << 31) ? f0 : 0.0;
         const double corr_i = strang ? 0.5 * ri.d : ri.d;
         double w1 = 0.0, w2 = 0.0;
         uint64_t wj = 0;
@@ -212,14 +216,21 @@ void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
             double b1[32], b2[32];
             uint64_t bj[32];
             for (int s = 0; s < 32; ++s) { b1[s] = 0.0; b2[s] = 0.0; bj[s] = 0; }
+            uint32_t n0 = 0; /* never-jumpers of this part */
             for (uint64_t c = wi; c < nch; c += wpr) {
                 for (int q = 0; q < 4; ++q) {
                     for (int s = 0; s < 32; ++s) {
                         const uint64_t l = c * 128 + 32 * q + s;
                         if (l >= W) continue;
                         uint64_t jl = 0;
-                        const double dev = fm_walker(rec, nbr, thr, alias, i, l, T0, f0, corr_i,
-                                                     dt, inv_dt, n_grid, N, strang, k0, k1, &jl);
+                        int jumped = 0;
+                        const double dev = fm_walker(rec, nbr, thr, alias, i, l, T0, K, corr_i,
+                                                     dt, inv_dt, n_grid, N, strang, k0, k1, &jl,
+                                                     &jumped);
+                        if (!jumped) {
+                            ++n0;
+                            continue; /* exact zero: skipped (bit-identical) */
+                        }
                         b1[s] = b1[s] + dev;
                         b2[s] = fma(dev, dev, b2[s]);
                         bj[s] += jl;
@@ -238,11 +249,18 @@ void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
                 memcpy(b2, c2, sizeof(c2));
                 memcpy(bj, cj, sizeof(cj));
             }
+            /* never-jumpers score f0: deviation f0 - K each, added after the
+             * butterfly (exactly zero when K = f0) */
+            const double cdev = f0 - K;
+            if (n0 != 0 && cdev != 0.0) {
+                b1[0] = fma((double)n0, cdev, b1[0]);
+                b2[0] = fma((double)n0, cdev * cdev, b2[0]);
+            }
             if (wi == 0) { w1 = b1[0]; w2 = b2[0]; wj = bj[0]; }
             else { w1 = w1 + b1[0]; w2 = w2 + b2[0]; wj += bj[0]; }
         }
         const double Wd = (double)W;
-        value[r] = f0 + w1 / Wd;
+        value[r] = K + w1 / Wd;
         double sev = 0.0;
         if (W > 1) {
             double var = (w2 - (w1 * w1) / Wd) / (Wd - 1.0);

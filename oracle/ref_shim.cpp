@@ -24,6 +24,7 @@
 
 #include "expmc/estimator.hpp"
 #include "expmc/generators.hpp"
+#include "expmc/metrics.hpp"
 #include "expmc/rng.hpp"
 #include "expmc/sampler.hpp"
 #include "expmc/sparse_matrix.hpp"
@@ -257,6 +258,26 @@ int ref_tc_estimate(void* h, double beta, std::uint64_t n_steps,
         *value = e.value;
         *se = e.std_error;
         *jumps = e.total_jumps;
+    });
+}
+
+// --- ranking metrics (metrics.cpp:10-55) ---------------------------------
+int ref_rank(const double* values, std::uint64_t n, std::uint32_t* order) {
+    return guarded([&] {
+        RankedVector r = rank(std::span<const double>(values, n));
+        std::memcpy(order, r.order.data(), n * 4);
+    });
+}
+
+int ref_isim(const std::uint32_t* ox, const std::uint32_t* oy, std::uint64_t nx,
+             std::uint64_t ny, double top_fraction, double* out) {
+    return guarded([&] {
+        RankedVector x, y;
+        x.order.assign(ox, ox + nx);
+        y.order.assign(oy, oy + ny);
+        x.scores.assign(nx, 0.0);
+        y.scores.assign(ny, 0.0);
+        *out = isim(x, y, top_fraction);
     });
 }
 

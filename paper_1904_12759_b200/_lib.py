@@ -36,6 +36,9 @@ SIGNATURES = [
     ("expmc_cuda_abi_version", C.c_int, []),
     ("expmc_cuda_create_from_csr", C.c_int,
      [C.c_uint64, u64p, u32p, f64p, f64p, C.c_int, C.POINTER(vp)]),
+    ("expmc_cuda_rank", C.c_int, [f64p, C.c_uint64, C.c_int, u32p]),
+    ("expmc_cuda_isim", C.c_int,
+     [u32p, u32p, C.c_uint64, C.c_uint64, C.c_double, C.c_int, f64p]),
     ("expmc_cuda_create_from_entries", C.c_int,
      [C.c_uint64, u32p, u32p, f64p, C.c_uint64, C.c_int, C.POINTER(vp)]),
     ("expmc_cuda_create_from_split", C.c_int,

@@ -636,6 +636,42 @@ int expmc_cuda_create_from_csr(uint64_t n, const uint64_t* row_ptr, const uint32
     });
 }
 
+int expmc_cuda_rank(const double* scores, uint64_t n, int device, uint32_t* order) {
+    // rank(), proj/src/metrics.cpp:10-25
+    return guarded([&] {
+        if (n >= (1ull << 31)) throw InvalidArg("rank: at most 2^31 scores");
+        if (n && (!scores || !order)) throw InvalidArg("rank: null array");
+        DeviceGuard g(device);
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        const bool ok = rank_device(scores, n, order, s);
+        after_launch(2);
+        cudaStreamDestroy(s);
+        if (!ok) throw InvalidArg("rank: NaN score");
+    });
+}
+
+int expmc_cuda_isim(const uint32_t* order_x, const uint32_t* order_y, uint64_t nx, uint64_t ny,
+                    double top_fraction, int device, double* out) {
+    // isim(), proj/src/metrics.cpp:27-55 (same checks and messages)
+    return guarded([&] {
+        if (nx != ny) throw InvalidArg("isim: length mismatch");
+        if (!(top_fraction > 0.0) || top_fraction > 1.0)
+            throw InvalidArg("isim: top_fraction must be in (0, 1]");
+        if (nx == 0) throw InvalidArg("isim: empty ranking");
+        if (nx >= (1ull << 31)) throw InvalidArg("isim: at most 2^31 nodes");
+        for (uint64_t i = 0; i < nx; ++i)
+            if (order_x[i] >= nx || order_y[i] >= nx) throw InvalidArg("isim: order out of range");
+        const uint64_t k = (uint64_t)std::ceil(top_fraction * (double)nx);
+        DeviceGuard g(device);
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        *out = isim_device(order_x, order_y, nx, k, s);
+        after_launch(5);
+        cudaStreamDestroy(s);
+    });
+}
+
 int expmc_cuda_create_from_entries(uint64_t n, const uint32_t* rows, const uint32_t* cols,
                                    const double* w, uint64_t ne, int device, expmc_matrix** out) {
     // SparseSymmetric::from_entries (sparse_matrix.cpp:18-85) on the device

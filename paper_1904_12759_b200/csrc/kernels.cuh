@@ -83,6 +83,11 @@ void from_entries_device(uint64_t n, const uint32_t* r, const uint32_t* c, const
                          double* diag, uint64_t* nnz_out, unsigned long long* err_host,
                          unsigned long long* dup_key, cudaStream_t s);
 
+// metrics.cu (§8f f4)
+bool rank_device(const double* scores_host, uint64_t n, uint32_t* order_host, cudaStream_t s);
+double isim_device(const uint32_t* ox_host, const uint32_t* oy_host, uint64_t n, uint64_t k,
+                   cudaStream_t s);
+
 // scatter_sort.cu
 size_t scatter_sort_temp_bytes(uint64_t batch, uint64_t n);
 void scatter_sort_accumulate(uint32_t* end, double* f, uint32_t* end_sorted, double* f_sorted,

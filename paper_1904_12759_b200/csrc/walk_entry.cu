@@ -61,7 +61,10 @@ struct RowConst {    // per task: the start row and its constants
     uint32_t chunk;  // chunk index (ChunkMeta only)
     unsigned long long T0;  // never-jump threshold on a u32 draw
     RowRec rr;       // record of the row
-    double f0;       // e^{β d_i} v_i
+    double f0;       // e^{β d_i} v_i (score of a walker that never jumps)
+    double K;        // shift of the deviation sums: f0 when never-jumpers are the
+                     // majority (T0 >= 2^31), else 0 (no cancellation against a
+                     // huge f0 that no walker realises, e.g. BA hubs)
     double corr;     // weight correction at the start state (½ d_i Strang, d_i Lie)
 };
 
@@ -117,6 +120,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             a.i = i;
             a.T0 = (unsigned long long)__dmul_rn(p0, 4294967296.0);
             a.f0 = __dmul_rn(exp_det(__dmul_rn(p.beta, ri.d)), ri.v);
+            a.K = a.T0 >= (1ull << 31) ? a.f0 : 0.0;
             a.corr = p.strang ? __dmul_rn(0.5, ri.d) : ri.d;
         }
         __syncwarp();
@@ -133,6 +137,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     // per-task accumulators (tasks finalize in order)
     double s1 = 0.0, s2 = 0.0;
     unsigned long long jsum = 0;
+    uint32_t nwt = 0, njt = 0;  // walkers / jumpers of the task part (warp-uniform)
 
     // One sojourn of the lane's walker from its current state: either the
     // path ends (park S', v, jumps in the ticket; lane becomes idle) or the
@@ -251,7 +256,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             if ((int)(head - te) < 0 ||
                 __ballot_sync(FULL, act && tk - ts < te - ts) != 0)
                 break;
-            const double f0 = m.row.f0, corr = m.row.corr;
+            const double f0 = m.row.f0, K = m.row.K, corr = m.row.corr;
             const uint64_t base = (uint64_t)m.row.chunk * kChunk;
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) q.dev[32 * qq + lane] = 0.0;
@@ -260,7 +265,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             for (uint32_t k = ts + lane; k < te; k += 32) {
                 const uint32_t pos = k & (CAP - 1);
                 const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], corr));
-                q.dev[q.rs[pos] & 255u] = __dsub_rn(__dmul_rn(exp_det(x), q.v[pos]), f0);
+                q.dev[q.rs[pos] & 255u] = __dsub_rn(__dmul_rn(exp_det(x), q.v[pos]), K);
                 jl += q.w[pos];
             }
             __syncwarp();
@@ -274,6 +279,8 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 }
             }
             jsum += jl;
+            njt += te - ts;
+            nwt += (uint32_t)(p.W - base < (uint64_t)kChunk ? p.W - base : (uint64_t)kChunk);
             if (m.last) {
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
@@ -282,10 +289,17 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                     jsum += __shfl_xor_sync(FULL, jsum, o);
                 }
                 if (lane == 0) {
+                    // never-jumpers score f0: deviation f0 - K each (0 when K = f0)
+                    const uint32_t n0 = nwt - njt;
+                    const double c = __dsub_rn(f0, K);
+                    if (n0 != 0 && c != 0.0) {
+                        s1 = __fma_rn((double)n0, c, s1);
+                        s2 = __fma_rn((double)n0, __dmul_rn(c, c), s2);
+                    }
                     const uint64_t task = m.task;
                     if (WPR == 1) {
                         const double W = (double)p.W;
-                        out_value[task] = __dadd_rn(f0, __ddiv_rn(s1, W));
+                        out_value[task] = __dadd_rn(K, __ddiv_rn(s1, W));
                         double se = 0.0;
                         if (p.W > 1) {
                             double var =
@@ -298,12 +312,14 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                         out_jumps[task] = jsum;
                     } else {
                         partial[task] = make_double4(s1, s2, __longlong_as_double((long long)jsum),
-                                                     f0);
+                                                     K);
                     }
                 }
                 s1 = 0.0;
                 s2 = 0.0;
                 jsum = 0;
+                nwt = 0;
+                njt = 0;
             }
             __syncwarp();
             oldest = (oldest + 1) & (R - 1);
@@ -324,7 +340,7 @@ __global__ void combine_parts_kernel(const double4* __restrict__ partial, uint64
     const double4 a = partial[r * WPR];
     double s1 = a.x, s2 = a.y;
     unsigned long long js = (unsigned long long)__double_as_longlong(a.z);
-    const double f0 = a.w;
+    const double K = a.w;
 #pragma unroll
     for (int k = 1; k < WPR; ++k) {
         const double4 b = partial[r * WPR + k];
@@ -333,7 +349,7 @@ __global__ void combine_parts_kernel(const double4* __restrict__ partial, uint64
         js += (unsigned long long)__double_as_longlong(b.z);
     }
     const double Wd = (double)W;
-    out_value[r] = __dadd_rn(f0, __ddiv_rn(s1, Wd));
+    out_value[r] = __dadd_rn(K, __ddiv_rn(s1, Wd));
     double se = 0.0;
     if (W > 1) {
         double var = __ddiv_rn(__dsub_rn(s2, __ddiv_rn(__dmul_rn(s1, s1), Wd)), __dsub_rn(Wd, 1.0));

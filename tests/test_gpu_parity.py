@@ -355,6 +355,55 @@ def test_cpp_header_api_runs(tmp_path, pb):
     assert "api_demo ok" in r.stdout
 
 
+def test_hub_rows_no_cancellation(pb, ref, orc):
+    """Rows where every walker jumps but e^{beta d_i} is astronomically large
+    (BA hubs, beta*d_max >> 1 as in config 5): the deviation shift must not
+    be f0 (regression: catastrophic cancellation).  GPU == model bit-exact,
+    and statistically equal to the reference."""
+    csr = pb.gen_ba(3000, 8, 1)
+    m = pb.split(csr)
+    s = orc.split(csr)
+    v = pb.gen_vector(1, csr.n, 2)
+    deg = np.diff(csr.row_ptr.astype(np.int64))
+    rows = np.sort(np.argsort(-deg)[:24]).astype(np.uint32)
+    beta, N, W = 2.0, 512, 2000  # beta * d_max ~ 500: f0 ~ e^500
+    got = pb.entries_estimate(m, v, rows, pb.PathParams(beta, N, W, pb.Splitting.Strang, 5))
+    mv, ms, mj = orc.fast_entries(s, v, rows, beta, N, W, 1, 5, pb.entry_slots(W))
+    assert np.array_equal(got.values, mv) and np.array_equal(got.jumps, mj)
+    assert np.all(np.isfinite(got.values)) and np.all(np.isfinite(got.std_errors))
+    rm = ref.matrix_from_csr(csr)
+    rv, rse, _ = rm.entries(v, rows, beta, N, W, 1, 6, workers=1, threads=8)
+    z = (got.values - rv) / np.sqrt(got.std_errors ** 2 + rse ** 2)
+    assert np.all(np.abs(z) < 5.0), z
+
+
+def test_rank_and_isim_match_reference(pb, ref):
+    """§8f f4: rank identical to the reference (ties, -0.0), isim to 1e-12."""
+    from paper_1904_12759_b200 import metrics
+
+    rng = np.random.default_rng(8)
+    for n in (1, 10, 1000, 200_000):
+        s = np.round(rng.normal(size=n), 2)  # many ties
+        s[: min(n, 3)] = [0.0, -0.0, 0.0][: min(n, 3)]
+        assert np.array_equal(metrics.rank(s), ref.rank(s))
+    x = rng.normal(size=50_000)
+    y = x + 0.3 * rng.normal(size=50_000)
+    ox, oy = ref.rank(x), ref.rank(y)
+    for frac in (1e-4, 0.01, 0.1, 1.0):
+        a, b = metrics.isim(ox, oy, frac), ref.isim(ox, oy, frac)
+        assert abs(a - b) <= 1e-12 * max(1.0, abs(b)), (frac, a, b)
+    import oracle
+
+    with pytest.raises(ValueError, match="rank: NaN score"):
+        metrics.rank([1.0, np.nan])
+    for args, msg in (((ox, oy[:-1], 0.1), "isim: length mismatch"),
+                      ((ox, oy, 0.0), r"isim: top_fraction must be in \(0, 1\]")):
+        with pytest.raises(ValueError, match=msg):
+            metrics.isim(*args)
+        with pytest.raises(oracle.RefError, match=msg):
+            ref.isim(*args)
+
+
 def test_from_entries_on_device_matches_reference(pb, ref):
     """§8f f1: GPU from_entries + split is bit-exact with the reference's
     SparseSymmetric::from_entries + split (shuffled, mixed triangles)."""
