@@ -45,6 +45,7 @@ struct FastParams {
     // Philox round keys (k0 + r W0, k1 + r W1), precomputed on the host so the
     // rounds read them as constant-bank operands instead of registers.
     PhiloxKeys rk;
+    unsigned long long* stats = nullptr;  // ENTRY_STATS builds only
 };
 
 // split_pack.cu

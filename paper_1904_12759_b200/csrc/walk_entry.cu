@@ -34,6 +34,8 @@
 //    l ≡ s (mod 32) with floor(l/128) ≡ w (mod WPR) in increasing l; lanes are
 //    combined by an xor butterfly, parts in index order.  Independent of
 //    scheduling, grid shape, GPU count and row sharding.
+#include <cstdio>
+
 #include "kernels.cuh"
 
 namespace expmc_b200 {
@@ -73,6 +75,7 @@ struct ChunkMeta {
     uint32_t tstart, tend;  // the chunk's ticket range (counters)
     uint32_t task;          // task id
     uint32_t last;          // last chunk of its task
+    uint32_t jm[4];         // jumper bitmask of slots 32q + lane (sweep ballots)
 };
 
 template <int R, int CAP>
@@ -85,6 +88,11 @@ struct WarpState {
     ChunkMeta meta[R];
     RowConst adm;       // row of the task being admitted
 };
+
+#ifdef ENTRY_STATS
+// [0] iterations [1] idle lanes at pop [2] lanes left idle [3] ...while
+// tasks remain (ring capacity) [4] jumping lanes [5] active lanes
+#endif
 
 template <int WPR>
 __global__ void __launch_bounds__(128, ENTRY_MIN_BLOCKS)
@@ -183,11 +191,13 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                     U4{0xffffffffu, base + (uint32_t)lane, q.adm.i, kTagEntry}, p.rk);
                 const uint32_t wd[4] = {D.x, D.y, D.z, D.w};
                 const uint32_t t0 = tail;
+                unsigned bq[4];
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
                     const uint32_t sl = 32u * qq + lane;
                     const bool jmp = (uint64_t)(base + sl) < p.W && (uint64_t)wd[qq] >= T0;
                     const unsigned b = __ballot_sync(FULL, jmp);
+                    bq[qq] = b;
                     if (jmp) {
                         const uint32_t pos = (tail + __popc(b & lt)) & (CAP - 1);
                         q.w[pos] = wd[qq];
@@ -204,6 +214,8 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                     m.tend = tail;
                     m.task = atask;
                     m.last = nextc >= nch;
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) m.jm[qq] = bq[qq];
                 }
                 __syncwarp();
                 ++live;
@@ -234,7 +246,27 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 sojourn(fin, jmp);
             }
             head += take;
+#ifdef ENTRY_STATS
+            if (lane == 0) {
+                atomicAdd(p.stats + 1, (unsigned long long)nidle);
+                if (avail < nidle) {  // lanes left idle: why?
+                    atomicAdd(p.stats + 2, (unsigned long long)(nidle - avail));
+                    if (atask < ntask) atomicAdd(p.stats + 3, 1ull);  // ring full
+                }
+            }
+#endif
         }
+#ifdef ENTRY_STATS
+        {
+            const unsigned jb = __ballot_sync(FULL, jmp);
+            const unsigned ab = __ballot_sync(FULL, act);
+            if (lane == 0) {
+                atomicAdd(p.stats + 0, 1ull);
+                atomicAdd(p.stats + 4, (unsigned long long)__popc(jb));
+                atomicAdd(p.stats + 5, (unsigned long long)__popc(ab));
+            }
+        }
+#endif
         // ---- C: one jump for every walker whose sojourn did not end the path
         if (jmp) {
             const ChunkMeta& m = q.meta[rsl >> 8];
@@ -258,9 +290,6 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 break;
             const double f0 = m.row.f0, K = m.row.K, corr = m.row.corr;
             const uint64_t base = (uint64_t)m.row.chunk * kChunk;
-#pragma unroll
-            for (int qq = 0; qq < 4; ++qq) q.dev[32 * qq + lane] = 0.0;
-            __syncwarp();
             unsigned long long jl = 0;
             for (uint32_t k = ts + lane; k < te; k += 32) {
                 const uint32_t pos = k & (CAP - 1);
@@ -272,7 +301,8 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
                 const uint32_t sl = 32u * qq + lane;
-                if (base + sl < p.W) {
+                // non-jumper slots contribute exact zeros: skipped (bit-identical)
+                if ((m.jm[qq] >> lane) & 1u) {
                     const double dv = q.dev[sl];
                     s1 = __dadd_rn(s1, dv);
                     s2 = __fma_rn(dv, dv, s2);
@@ -395,11 +425,31 @@ int launch_entry_fast(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
                       void* scratch, cudaStream_t s) {
     if (nrows == 0) return 0;
     double4* part = static_cast<double4*>(scratch);
+#ifdef ENTRY_STATS
+    static unsigned long long* st = nullptr;
+    if (!st) cudaMallocManaged(&st, 64);
+    cudaStreamSynchronize(s);
+    for (int z = 0; z < 8; ++z) st[z] = 0;
+    FastParams ps = p;
+    ps.stats = st;
+#define p ps
+#endif
+    int k;
     switch (entry_fast_wpr(p.W)) {
-        case 4: return launch_t<4>(m, rows, nrows, p, value, se, jumps, part, s);
-        case 2: return launch_t<2>(m, rows, nrows, p, value, se, jumps, part, s);
-        default: return launch_t<1>(m, rows, nrows, p, value, se, jumps, part, s);
+        case 4: k = launch_t<4>(m, rows, nrows, p, value, se, jumps, part, s); break;
+        case 2: k = launch_t<2>(m, rows, nrows, p, value, se, jumps, part, s); break;
+        default: k = launch_t<1>(m, rows, nrows, p, value, se, jumps, part, s); break;
     }
+#ifdef ENTRY_STATS
+#undef p
+    cudaStreamSynchronize(s);
+    fprintf(stderr,
+            "ENTRY_STATS iters %llu idle@pop %.2f left_idle %.2f ring_full_iters %.3f "
+            "jump_lanes %.2f active %.2f\n",
+            st[0], (double)st[1] / st[0], (double)st[2] / st[0], (double)st[3] / st[0],
+            (double)st[4] / st[0], (double)st[5] / st[0]);
+#endif
+    return k;
 }
 
 }  // namespace expmc_b200
