@@ -142,7 +142,7 @@ struct expmc_matrix {
     DevSplit m;
     std::vector<void*> owned;
     DevBuf vdev, rows, out_val, out_se, out_j, fa, vcum, values, pa, pb, pc, scal, tmp1, tmp2,
-        tmp3, iota, part, fa2, sort_tmp;
+        tmp3, iota, part, fa2, sort_tmp, lens;
     uint64_t iota_n = 0;
     // host copies kept for K5 norm bounds
     std::vector<double> h_rate, h_diag;
@@ -157,7 +157,7 @@ struct expmc_matrix {
     ~expmc_matrix() {
         for (void* p : owned) cudaFree(p);
         for (DevBuf* b : {&vdev, &rows, &out_val, &out_se, &out_j, &fa, &vcum, &values, &pa,
-                          &pb, &pc, &scal, &tmp1, &tmp2, &tmp3, &iota, &part, &fa2, &sort_tmp})
+                          &pb, &pc, &scal, &tmp1, &tmp2, &tmp3, &iota, &part, &fa2, &sort_tmp, &lens})
             b->release();
         if (stream) cudaStreamDestroy(stream);
         if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -497,8 +497,8 @@ void run_scatter(expmc_matrix* h, int start_mode, const std::vector<double>* cum
         rec_f = h->tmp2.get<double>(B * 2);
         f_sorted = rec_f + B;
         run_keys = h->tmp3.get<uint32_t>(B + 2);
+        nruns = h->lens.get<int>(2 * (B + 1) + 2);
         run_sums = h->fa2.get<double>(B);
-        nruns = reinterpret_cast<int*>(run_keys + B);
         temp_bytes = scatter_sort_temp_bytes(B, n);
         temp = h->sort_tmp.get<unsigned char>(temp_bytes);
     }

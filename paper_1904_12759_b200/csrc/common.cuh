@@ -165,23 +165,33 @@ __device__ __forceinline__ float neg_ln_u(uint32_t w) {
 // model (oracle/fast_model.c fm_exp) reproduces it bit for bit: Cody-Waite
 // reduction x = n ln2 + r, |r| <= ln2/2, degree-13 Taylor for e^r, exact
 // scaling by 2^n.  Max error ~1 ulp on [-745, 709.78].
+// Coefficients in the constant bank: DFMA reads them as c[][] operands
+// instead of materialising each 64-bit literal with two UMOVs.
+#ifdef EXP_DET_LITERAL
+#define EXPC(k) (kExpDet[k])
+constexpr double kExpDet[16] = {
+#else
+#define EXPC(k) (c_exp_det[k])
+__constant__ double c_exp_det[16] = {
+#endif
+    1.4426950408889634,         // log2(e)
+    6.93147180369123816490e-01, // ln2 hi
+    1.90821492927058770002e-10, // ln2 lo
+    1.6059043836821614599e-10,  // 1/13!
+    2.0876756987868098979e-09, 2.5052108385441718775e-08, 2.7557319223985890653e-07,
+    2.7557319223985890653e-06, 2.4801587301587301566e-05, 1.9841269841269841253e-04,
+    1.3888888888888889419e-03, 8.3333333333333332177e-03, 4.1666666666666664354e-02,
+    1.6666666666666665741e-01, 709.782712893384, -745.1332191019412};
+
 __device__ __forceinline__ double exp_det(double x) {
-    if (!(x < 709.782712893384)) return x != x ? x : __longlong_as_double(0x7ff0000000000000LL);
-    if (x < -745.1332191019412) return 0.0;
-    const double n = rint(__dmul_rn(x, 1.4426950408889634));
-    double r = __fma_rn(-n, 6.93147180369123816490e-01, x);
-    r = __fma_rn(-n, 1.90821492927058770002e-10, r);
-    double q = 1.6059043836821614599e-10;  // 1/13!
-    q = __fma_rn(q, r, 2.0876756987868098979e-09);
-    q = __fma_rn(q, r, 2.5052108385441718775e-08);
-    q = __fma_rn(q, r, 2.7557319223985890653e-07);
-    q = __fma_rn(q, r, 2.7557319223985890653e-06);
-    q = __fma_rn(q, r, 2.4801587301587301566e-05);
-    q = __fma_rn(q, r, 1.9841269841269841253e-04);
-    q = __fma_rn(q, r, 1.3888888888888889419e-03);
-    q = __fma_rn(q, r, 8.3333333333333332177e-03);
-    q = __fma_rn(q, r, 4.1666666666666664354e-02);
-    q = __fma_rn(q, r, 1.6666666666666665741e-01);
+    if (!(x < EXPC(14))) return x != x ? x : __longlong_as_double(0x7ff0000000000000LL);
+    if (x < EXPC(15)) return 0.0;
+    const double n = rint(__dmul_rn(x, EXPC(0)));
+    double r = __fma_rn(-n, EXPC(1), x);
+    r = __fma_rn(-n, EXPC(2), r);
+    double q = EXPC(3);
+#pragma unroll
+    for (int k = 4; k < 14; ++k) q = __fma_rn(q, r, EXPC(k));
     q = __fma_rn(q, r, 0.5);
     q = __fma_rn(q, r, 1.0);
     q = __fma_rn(q, r, 1.0);
