@@ -88,6 +88,12 @@ int expmc_cuda_create_from_entries(uint64_t n, const uint32_t* rows, const uint3
 int expmc_cuda_create_from_split(uint64_t n, const uint64_t* row_offset,
                                  const uint32_t* neighbor, const double* weight,
                                  const double* diag, int device, expmc_matrix** out);
+/* From a Matrix Market coordinate file, exactly load_matrix_market
+ * (matrix_market.cpp:51-165): header rules and "path:line: what" messages
+ * as EXPMC_RUNTIME_ERROR; the body is parsed on all host cores, the
+ * general-symmetry fold and from_entries run on the device (from_entries'
+ * own messages as EXPMC_INVALID_ARGUMENT), then split() on the device. */
+int expmc_cuda_create_from_mm(const char* path, int device, expmc_matrix** out);
 int expmc_cuda_destroy(expmc_matrix* m);
 
 int expmc_cuda_matrix_info(const expmc_matrix* m, uint64_t* n, uint64_t* nnz, double* dbar,
@@ -187,6 +193,33 @@ int expmc_csr_export(const expmc_csr* c, uint64_t* row_ptr, uint32_t* col, doubl
 int expmc_csr_view(const expmc_csr* c, const uint64_t** row_ptr, const uint32_t** col,
                    const double** val, const double** diag);
 void expmc_csr_free(expmc_csr* c);
+
+/* ------------------------------------ Matrix Market + CSR cache (f1, f3) */
+/* load_matrix_market (matrix_market.cpp:51-165) into a host CSR (the
+ * SparseSymmetric adjacency); fold + from_entries on `device`.  Errors as
+ * expmc_cuda_create_from_mm, message in expmc_cuda_last_error(). */
+int expmc_cuda_mm_load(const char* path, int device, expmc_csr** out);
+/* The parse alone (matrix_market.cpp:51-131, host, all cores): entries in
+ * file order, 0-based, before the general fold / from_entries.  Message in
+ * expmc_gen_last_error(). */
+typedef struct expmc_mm expmc_mm;
+int expmc_mm_parse(const char* path, expmc_mm** out);
+int expmc_mm_info(const expmc_mm* m, uint64_t* n, uint64_t* n_entries, int32_t* general,
+                  int32_t* pattern, uint64_t* last_line);
+int expmc_mm_view(const expmc_mm* m, const uint32_t** rows, const uint32_t** cols,
+                  const double** weights);
+void expmc_mm_free(expmc_mm* m);
+/* write_matrix_market (matrix_market.cpp:167-194) of a mirrored CSR + diag
+ * (diag may be NULL): lower triangle, 1-based, shortest round-trip weights,
+ * `pattern` when every stored weight is 1. */
+int expmc_mm_write(const char* path, uint64_t n, const uint64_t* row_ptr, const uint32_t* col,
+                   const double* val, const double* diag);
+/* Binary CSR cache: 64-byte header ("EXPMCCSR", version 1, n, nnz,
+ * checksum) + row_ptr u64[n+1] + col u32[nnz] (8-byte padded) + val f64[nnz]
+ * + diag f64[n].  Load verifies size, checksum and row_ptr. */
+int expmc_csr_save(const char* path, uint64_t n, const uint64_t* row_ptr, const uint32_t* col,
+                   const double* val, const double* diag);
+int expmc_csr_load(const char* path, expmc_csr** out);
 /* Seeded vectors / row samples with PCG32 RngStream(seed, 0):
  *   kind 0: U[0,1)  1: U[-1,1)  2: 3-D Gaussian bump (sigma) + U[0,1) on a
  *   side^3 grid (row-major, cube [0,1]^3, centre 0.5) */

@@ -43,6 +43,28 @@ def _load(path):
     return C.CDLL(path)
 
 
+_MM_WRITE_CHILD = r"""
+import array, ctypes as C, sys
+L = C.CDLL(sys.argv[1])
+L.ref_from_entries.restype = C.c_void_p
+L.ref_from_entries.argtypes = [C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]
+L.ref_mm_write.argtypes = [C.c_void_p, C.c_char_p]
+L.ref_last_error.restype = C.c_char_p
+raw = open(sys.argv[2], "rb").read()
+hdr = array.array("Q"); hdr.frombytes(raw[:16]); n, ne = hdr
+o = 16
+r = array.array("I"); r.frombytes(raw[o:o + 4 * ne]); o += 4 * ne
+c = array.array("I"); c.frombytes(raw[o:o + 4 * ne]); o += 4 * ne
+w = array.array("d"); w.frombytes(raw[o:o + 8 * ne])
+buf = lambda a: (C.c_char * max(1, len(a) * a.itemsize)).from_buffer_copy(a.tobytes() or b"\0")
+h = L.ref_from_entries(n, buf(r), buf(c), buf(w), ne)
+if not h:
+    sys.exit(L.ref_last_error().decode())
+if L.ref_mm_write(h, sys.argv[3].encode()) != 0:
+    sys.exit(L.ref_last_error().decode())
+"""
+
+
 # ----------------------------------------------------------------- C oracle
 class Oracle:
     """ctypes view of liboracle.so."""
@@ -205,6 +227,9 @@ class Ref:
         L.ref_generate.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64,
                                    C.c_double, C.c_uint64]
         L.ref_destroy.argtypes = [C.c_void_p]
+        L.ref_mm_load.restype = C.c_void_p
+        L.ref_mm_load.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
+        L.ref_mm_write.argtypes = [C.c_void_p, C.c_char_p]
         L.ref_sizes.argtypes = [C.c_void_p, _u64p, _u64p]
         L.ref_split_export.argtypes = [C.c_void_p, _f64p, _f64p, _f64p, _u64p, _u32p, _f64p,
                                        _f64p, _u8p, _f64p, _u64p]
@@ -262,6 +287,41 @@ class Ref:
         if not h:
             raise RefError(self.L.ref_last_error().decode())
         return RefMatrix(self, h)
+
+    def mm_load(self, path):
+        """load_matrix_market; raises RefError with .kind 1 (invalid_argument)
+        or 2 (runtime_error)."""
+        st = C.c_int()
+        h = self.L.ref_mm_load(os.fsencode(path), C.byref(st))
+        if not h:
+            e = RefError(self.L.ref_last_error().decode())
+            e.kind = st.value
+            raise e
+        return RefMatrix(self, h)
+
+    def mm_write_entries(self, n, rows, cols, w, path):
+        """write_matrix_market of from_entries(n, entries), run in a child
+        interpreter without numpy: the reference's std::ofstream writer
+        crashes inside a process that has numpy's C++ runtime loaded first
+        (observed here), so the child loads only ctypes."""
+        import subprocess
+        import sys
+        import tempfile
+
+        with tempfile.NamedTemporaryFile(suffix=".bin", delete=False) as f:
+            np.array([n, len(w)], np.uint64).tofile(f)
+            np.ascontiguousarray(rows, np.uint32).tofile(f)
+            np.ascontiguousarray(cols, np.uint32).tofile(f)
+            np.ascontiguousarray(w, np.float64).tofile(f)
+            tmp = f.name
+        try:
+            r = subprocess.run([sys.executable, "-c", _MM_WRITE_CHILD,
+                                os.path.join(HERE, "_ref", "libexpmc_ref.so"), tmp,
+                                os.fspath(path)], capture_output=True, text=True)
+        finally:
+            os.unlink(tmp)
+        if r.returncode != 0:
+            raise RefError(r.stderr.strip() or f"writer exited {r.returncode}")
 
     def generate(self, kind, n, k=1, ps=0.0, m0=2, p=0.0, seed=0):
         h = self.L.ref_generate(kind, n, k, ps, m0, p, seed)

@@ -12,6 +12,7 @@
 //   entry_estimate                  proj/src/estimator.cpp:169-206
 //   vector_estimate                 proj/src/estimator.cpp:208-278
 //   tc_estimate                     proj/src/estimator.cpp:280-318
+//   load/write_matrix_market        proj/src/matrix_market.cpp:51-207
 //   RngStream / exp_time / advance  proj/include/expmc/rng.hpp:14-63,
 //                                   proj/src/sampler.cpp:10-49
 #include <atomic>
@@ -24,6 +25,7 @@
 
 #include "expmc/estimator.hpp"
 #include "expmc/generators.hpp"
+#include "expmc/matrix_market.hpp"
 #include "expmc/metrics.hpp"
 #include "expmc/rng.hpp"
 #include "expmc/sampler.hpp"
@@ -129,6 +131,27 @@ void* ref_generate(int kind, std::uint64_t n, std::uint64_t k, double ps,
         out = m;
     });
     return rc == 0 ? out : nullptr;
+}
+
+// load_matrix_market + split; *status: 0 ok, 1 invalid_argument, 2 other.
+void* ref_mm_load(const char* path, int* status) {
+    RefMatrix* out = nullptr;
+    *status = guarded([&] {
+        auto* m = new RefMatrix;
+        try {
+            m->sym = load_matrix_market(path);
+            m->split = split(m->sym);
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        out = m;
+    });
+    return out;
+}
+
+int ref_mm_write(void* h, const char* path) {
+    return guarded([&] { write_matrix_market(static_cast<RefMatrix*>(h)->sym, path); });
 }
 
 void ref_destroy(void* h) { delete static_cast<RefMatrix*>(h); }

@@ -8,9 +8,11 @@ The reference's estimator API (arXiv 1904.12759 C++ artifact,
 from ._lib import ExpmcError, lib
 from .estimator import (EntriesEstimate, Estimate, PathParams, Rng, SplitMatrix, Splitting,
                         VectorEstimate, entries_device, entries_estimate, entry_estimate,
-                        entry_slots, expmv, from_entries, gather_ceiling_device, launch_count, set_v_device,
+                        entry_slots, expmv, from_entries, from_matrix_market, gather_ceiling_device, launch_count, set_v_device,
                         split, splitting_product, tc_estimate, vector_estimate)
-from .inputs import Csr, build_config, csr_from_dense, gen_ba, gen_fd, gen_row_sample, gen_vector, gen_ws, n_rule
+from .inputs import (Csr, MmEntries, build_config, csr_from_dense, gen_ba, gen_fd, gen_row_sample,
+                     gen_vector, gen_ws, load_csr, load_matrix_market, n_rule, parse_matrix_market,
+                     save_csr, write_matrix_market)
 from .spectral import BetaRule, lambda_max, resolve_beta
 
 __all__ = [
@@ -19,5 +21,6 @@ __all__ = [
     "entry_slots", "expmv", "gather_ceiling_device", "launch_count", "set_v_device", "split",
     "splitting_product", "tc_estimate", "vector_estimate", "Csr", "build_config",
     "csr_from_dense", "gen_ba", "gen_fd", "gen_row_sample", "gen_vector", "gen_ws", "n_rule",
-    "BetaRule", "lambda_max", "resolve_beta",
+    "BetaRule", "lambda_max", "resolve_beta", "from_matrix_market", "MmEntries", "load_csr",
+    "load_matrix_market", "parse_matrix_market", "save_csr", "write_matrix_market",
 ]

@@ -43,6 +43,7 @@ SIGNATURES = [
      [C.c_uint64, u32p, u32p, f64p, C.c_uint64, C.c_int, C.POINTER(vp)]),
     ("expmc_cuda_create_from_split", C.c_int,
      [C.c_uint64, u64p, u32p, f64p, f64p, C.c_int, C.POINTER(vp)]),
+    ("expmc_cuda_create_from_mm", C.c_int, [C.c_char_p, C.c_int, C.POINTER(vp)]),
     ("expmc_cuda_destroy", C.c_int, [vp]),
     ("expmc_cuda_matrix_info", C.c_int,
      [vp, u64p, u64p, f64p, u64p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
@@ -75,6 +76,15 @@ SIGNATURES = [
     ("expmc_csr_export", C.c_int, [vp, u64p, u32p, f64p, f64p]),
     ("expmc_csr_view", C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     ("expmc_csr_free", None, [vp]),
+    ("expmc_cuda_mm_load", C.c_int, [C.c_char_p, C.c_int, C.POINTER(vp)]),
+    ("expmc_mm_parse", C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    ("expmc_mm_info", C.c_int,
+     [vp, u64p, u64p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), u64p]),
+    ("expmc_mm_view", C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
+    ("expmc_mm_free", None, [vp]),
+    ("expmc_mm_write", C.c_int, [C.c_char_p, C.c_uint64, u64p, u32p, f64p, f64p]),
+    ("expmc_csr_save", C.c_int, [C.c_char_p, C.c_uint64, u64p, u32p, f64p, f64p]),
+    ("expmc_csr_load", C.c_int, [C.c_char_p, C.POINTER(vp)]),
     ("expmc_gen_vector", C.c_int,
      [C.c_int, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64, f64p]),
     ("expmc_gen_row_sample", C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, u32p]),

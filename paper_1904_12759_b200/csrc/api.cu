@@ -11,9 +11,11 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "expmc_b200.h"
+#include "host_io.h"
 #include "kernels.cuh"
 
 using namespace expmc_b200;
@@ -349,6 +351,105 @@ expmc_matrix* build_device_csr(uint64_t n, uint64_t nnz, const uint64_t* row_ptr
     return h;
 }
 
+struct Stream {
+    cudaStream_t s = nullptr;
+    Stream() { CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+    ~Stream() {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+    }
+};
+
+// Device CSR produced by from_entries_device (owned here).
+struct DevCsr {
+    uint64_t* rp = nullptr;
+    uint32_t* col = nullptr;
+    double* val = nullptr;
+    double* diag = nullptr;
+    uint64_t nnz = 0;
+    ~DevCsr() {
+        cudaFree(rp); cudaFree(col); cudaFree(val); cudaFree(diag);
+    }
+};
+
+template <class T>
+struct DevArr {
+    T* p = nullptr;
+    ~DevArr() { cudaFree(p); }
+};
+
+// from_entries on device arrays; at(k) = (row, col) of input entry k, for the
+// reference's messages (sparse_matrix.cpp:20-51).
+template <class At>
+void device_from_entries(uint64_t n, const uint32_t* r_d, const uint32_t* c_d, const double* w_d,
+                         uint64_t ne, cudaStream_t s, At at, DevCsr& out) {
+    CK(cudaMalloc(&out.diag, (n ? n : 1) * 8));
+    CK(cudaMalloc(&out.rp, (n + 1) * 8));
+    unsigned long long err[2] = {~0ull, ~0ull}, dup = 0;
+    from_entries_device(n, r_d, c_d, w_d, ne, out.rp, &out.col, &out.val, out.diag, &out.nnz, err,
+                        &dup, s);
+    CK(cudaGetLastError());
+    if (err[0] != ~0ull) {
+        const auto e = at(err[0] >> 3);
+        const std::string es = "(" + std::to_string(e.first) + ", " + std::to_string(e.second) + ")";
+        switch ((int)(err[0] & 7)) {
+            case 1:
+                throw InvalidArg("entry " + es + " out of range for n = " + std::to_string(n));
+            case 2: throw InvalidArg("non-finite weight at " + es);
+            case 3: throw InvalidArg("explicit zero entry at " + es);
+            default:
+                throw InvalidArg("negative off-diagonal weight at " + es + ": no CTMC interpretation");
+        }
+    }
+    if (err[1] != ~0ull)
+        throw InvalidArg("duplicate entry at (" + std::to_string(dup >> 32) + ", " +
+                         std::to_string(dup & 0xffffffffull) + ")");
+    if (out.nnz >= (1ull << 32)) throw InvalidArg("nnz must be < 2^32");
+}
+
+// Host entry list -> device CSR.  general: fold both triangles first
+// (matrix_market.cpp:136-164; errors are "path:last_line: ..." runtime errors).
+void upload_and_convert(uint64_t n, const uint32_t* rows, const uint32_t* cols, const double* w,
+                        uint64_t ne, bool general, const std::string& path, uint64_t last_line,
+                        cudaStream_t s, DevCsr& out) {
+    DevArr<uint32_t> r_d, c_d;
+    DevArr<double> w_d;
+    CK(cudaMalloc(&r_d.p, (ne ? ne : 1) * 4));
+    CK(cudaMalloc(&c_d.p, (ne ? ne : 1) * 4));
+    CK(cudaMalloc(&w_d.p, (ne ? ne : 1) * 8));
+    if (ne) {
+        CK(cudaMemcpyAsync(r_d.p, rows, ne * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(c_d.p, cols, ne * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(w_d.p, w, ne * 8, cudaMemcpyHostToDevice, s));
+    }
+    if (!general) {
+        device_from_entries(n, r_d.p, c_d.p, w_d.p, ne, s,
+                            [&](uint64_t k) { return std::make_pair(rows[k], cols[k]); }, out);
+        return;
+    }
+    DevArr<uint32_t> fr, fc;
+    DevArr<double> fw;
+    uint64_t m = 0;
+    unsigned long long err = ~0ull, key = 0;
+    fold_general_device(r_d.p, c_d.p, w_d.p, ne, &fr.p, &fc.p, &fw.p, &m, &err, &key, s);
+    CK(cudaGetLastError());
+    if (err != ~0ull) {
+        const std::string at = "(" + std::to_string((key >> 32) + 1) + ", " +
+                               std::to_string((key & 0xffffffffull) + 1) + ")";
+        throw std::runtime_error(mm_message(path, last_line,
+                                            (err & 1) ? "general matrix is not symmetric at " + at
+                                                      : "duplicate diagonal entry " + at));
+    }
+    device_from_entries(n, fr.p, fc.p, fw.p, m, s,
+                        [&](uint64_t k) {
+                            uint32_t a = 0, b = 0;
+                            cudaMemcpy(&a, fr.p + k, 4, cudaMemcpyDeviceToHost);
+                            cudaMemcpy(&b, fc.p + k, 4, cudaMemcpyDeviceToHost);
+                            return std::make_pair(a, b);
+                        },
+                        out);
+}
+
 // Run the entry estimator for host rows / host v; outputs to host.
 void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* rows,
                  uint64_t nrows, const expmc_path_params* p, double* value, double* se,
@@ -681,58 +782,58 @@ int expmc_cuda_create_from_entries(uint64_t n, const uint32_t* rows, const uint3
         if (ne >= (1ull << 30)) throw InvalidArg("at most 2^30 entries");
         if (ne && (!rows || !cols || !w)) throw InvalidArg("entry arrays are null");
         DeviceGuard g(device);
-        cudaStream_t s;
-        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-        uint32_t *r_d = nullptr, *c_d = nullptr, *col = nullptr;
-        double *w_d = nullptr, *diag_d = nullptr, *val = nullptr;
-        uint64_t* rp_d = nullptr;
-        auto cleanup = [&] {
-            cudaFree(r_d); cudaFree(c_d); cudaFree(w_d); cudaFree(diag_d); cudaFree(rp_d);
-            cudaFree(col); cudaFree(val);
-            cudaStreamDestroy(s);
-        };
+        Stream s;
+        DevCsr csr;
+        upload_and_convert(n, rows, cols, w, ne, false, "", 0, s.s, csr);
+        *out = build_device_csr(n, csr.nnz, csr.rp, csr.col, csr.val, csr.diag, device);
+    });
+}
+
+int expmc_cuda_create_from_mm(const char* path, int device, expmc_matrix** out) {
+    // load_matrix_market (matrix_market.cpp:51-165) -> split, on the device
+    return guarded([&] {
+        if (!out) throw InvalidArg("out is null");
+        expmc_mm mm;
+        mm_parse(path, mm);
+        DeviceGuard g(device);
+        Stream s;
+        DevCsr csr;
+        upload_and_convert(mm.n, mm.r.data(), mm.c.data(), mm.w.data(), mm.r.size(), mm.general,
+                           mm.path, mm.last_line, s.s, csr);
+        *out = build_device_csr(mm.n, csr.nnz, csr.rp, csr.col, csr.val, csr.diag, device);
+    });
+}
+
+int expmc_cuda_mm_load(const char* path, int device, expmc_csr** out) {
+    // load_matrix_market -> the SparseSymmetric adjacency, back on the host
+    return guarded([&] {
+        if (!out) throw InvalidArg("out is null");
+        expmc_mm mm;
+        mm_parse(path, mm);
+        DeviceGuard g(device);
+        Stream s;
+        DevCsr csr;
+        upload_and_convert(mm.n, mm.r.data(), mm.c.data(), mm.w.data(), mm.r.size(), mm.general,
+                           mm.path, mm.last_line, s.s, csr);
+        auto* c = new expmc_csr;
         try {
-            CK(cudaMalloc(&r_d, (ne ? ne : 1) * 4));
-            CK(cudaMalloc(&c_d, (ne ? ne : 1) * 4));
-            CK(cudaMalloc(&w_d, (ne ? ne : 1) * 8));
-            CK(cudaMalloc(&diag_d, (n ? n : 1) * 8));
-            CK(cudaMalloc(&rp_d, (n + 1) * 8));
-            if (ne) {
-                CK(cudaMemcpyAsync(r_d, rows, ne * 4, cudaMemcpyHostToDevice, s));
-                CK(cudaMemcpyAsync(c_d, cols, ne * 4, cudaMemcpyHostToDevice, s));
-                CK(cudaMemcpyAsync(w_d, w, ne * 8, cudaMemcpyHostToDevice, s));
+            c->n = mm.n;
+            c->row_ptr.resize(mm.n + 1);
+            c->col.resize(csr.nnz);
+            c->val.resize(csr.nnz);
+            c->diag.resize(mm.n);
+            CK(cudaMemcpyAsync(c->row_ptr.data(), csr.rp, (mm.n + 1) * 8, cudaMemcpyDeviceToHost, s.s));
+            CK(cudaMemcpyAsync(c->diag.data(), csr.diag, mm.n * 8, cudaMemcpyDeviceToHost, s.s));
+            if (csr.nnz) {
+                CK(cudaMemcpyAsync(c->col.data(), csr.col, csr.nnz * 4, cudaMemcpyDeviceToHost, s.s));
+                CK(cudaMemcpyAsync(c->val.data(), csr.val, csr.nnz * 8, cudaMemcpyDeviceToHost, s.s));
             }
-            uint64_t nnz = 0;
-            unsigned long long err[2] = {~0ull, ~0ull}, dup = 0;
-            from_entries_device(n, r_d, c_d, w_d, ne, rp_d, &col, &val, diag_d, &nnz, err, &dup,
-                                s);
-            CK(cudaGetLastError());
-            auto raw = [&](uint64_t k) {  // entry_str of the input entry
-                return "(" + std::to_string(rows[k]) + ", " + std::to_string(cols[k]) + ")";
-            };
-            if (err[0] != ~0ull) {
-                const uint64_t k = err[0] >> 3;
-                switch ((int)(err[0] & 7)) {
-                    case 1:
-                        throw InvalidArg("entry " + raw(k) + " out of range for n = " +
-                                         std::to_string(n));
-                    case 2: throw InvalidArg("non-finite weight at " + raw(k));
-                    case 3: throw InvalidArg("explicit zero entry at " + raw(k));
-                    default:
-                        throw InvalidArg("negative off-diagonal weight at " + raw(k) +
-                                         ": no CTMC interpretation");
-                }
-            }
-            if (err[1] != ~0ull)
-                throw InvalidArg("duplicate entry at (" + std::to_string(dup >> 32) + ", " +
-                                 std::to_string(dup & 0xffffffffull) + ")");
-            if (nnz >= (1ull << 32)) throw InvalidArg("nnz must be < 2^32");
-            *out = build_device_csr(n, nnz, rp_d, col, val, diag_d, device);
+            CK(cudaStreamSynchronize(s.s));
         } catch (...) {
-            cleanup();
+            delete c;
             throw;
         }
-        cleanup();
+        *out = c;
     });
 }
 

@@ -12,6 +12,9 @@
 // Integer work throughout: bit-exact with the reference.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+
+#include <algorithm>
 
 #include "kernels.cuh"
 
@@ -94,7 +97,102 @@ __global__ void deg_to_u64_kernel(const unsigned int* __restrict__ deg, uint64_t
 
 inline unsigned blocks(uint64_t x) { return (unsigned)((x + 255) / 256); }
 
+// General-symmetry fold (matrix_market.cpp:136-164) over canonical keys
+// sorted by (row, col): a run start is kept; a diagonal run must have length
+// 1, an off-diagonal run length 2 with equal weights.  First failing run in
+// sorted order -> err (sorted position << 1 | kind; kind 0 = duplicate
+// diagonal, 1 = not symmetric).
+__global__ void fold_check_kernel(const unsigned long long* __restrict__ key,
+                                  const uint64_t* __restrict__ idx, const double* __restrict__ w,
+                                  uint64_t ne, unsigned char* __restrict__ keep,
+                                  unsigned long long* __restrict__ err) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= ne) return;
+    const unsigned long long x = key[k];
+    const bool start = k == 0 || key[k - 1] != x;
+    keep[k] = start;
+    if (!start) return;
+    const bool has2 = k + 1 < ne && key[k + 1] == x;
+    if ((uint32_t)(x >> 32) == (uint32_t)x) {
+        if (has2) atomicMin(err, (unsigned long long)k << 1);
+    } else {
+        const bool has3 = k + 2 < ne && key[k + 2] == x;
+        if (!has2 || has3 || w[idx[k]] != w[idx[k + 1]])
+            atomicMin(err, ((unsigned long long)k << 1) | 1ull);
+    }
+}
+
+__global__ void fold_unpack_kernel(const unsigned long long* __restrict__ key,
+                                   const uint64_t* __restrict__ idx,
+                                   const double* __restrict__ w, uint64_t m,
+                                   uint32_t* __restrict__ r, uint32_t* __restrict__ c,
+                                   double* __restrict__ fw) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    r[k] = (uint32_t)(key[k] >> 32);
+    c[k] = (uint32_t)key[k];
+    fw[k] = w[idx[k]];
+}
+
 }  // namespace
+
+// Fold a general (two-triangle) entry list into its upper triangle on the
+// device.  On success r_out / c_out / w_out hold *m entries (device memory
+// owned by the caller), sorted by (row, col) with row <= col.  On failure
+// *err_host = sorted position << 1 | kind and *err_key = that run's
+// canonical key; outputs are left null.
+void fold_general_device(const uint32_t* r, const uint32_t* c, const double* w, uint64_t ne,
+                         uint32_t** r_out, uint32_t** c_out, double** w_out, uint64_t* m,
+                         unsigned long long* err_host, unsigned long long* err_key,
+                         cudaStream_t s) {
+    *r_out = nullptr;
+    *c_out = nullptr;
+    *w_out = nullptr;
+    *m = 0;
+    *err_host = ~0ull;
+    if (ne == 0) return;
+    unsigned long long *key, *key2, *err;
+    uint64_t *idx, *idx2;
+    unsigned char* keep;
+    int* nsel;
+    cudaMalloc(&key, ne * 8);
+    cudaMalloc(&key2, ne * 8);
+    cudaMalloc(&idx, ne * 8);
+    cudaMalloc(&idx2, ne * 8);
+    cudaMalloc(&keep, ne);
+    cudaMalloc(&err, 8);
+    cudaMalloc(&nsel, 4);
+    cudaMemcpyAsync(err, err_host, 8, cudaMemcpyHostToDevice, s);
+    canon_kernel<<<blocks(ne), 256, 0, s>>>(r, c, ne, key, idx);
+    size_t tb = 0, tk = 0, ti = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key2, idx, idx2, (int)ne, 0, 64, s);
+    cub::DeviceSelect::Flagged(nullptr, tk, key2, keep, key, nsel, (int)ne, s);
+    cub::DeviceSelect::Flagged(nullptr, ti, idx2, keep, idx, nsel, (int)ne, s);
+    void* tmp = nullptr;
+    cudaMalloc(&tmp, std::max(tb, std::max(tk, ti)));
+    cub::DeviceRadixSort::SortPairs(tmp, tb, key, key2, idx, idx2, (int)ne, 0, 64, s);
+    fold_check_kernel<<<blocks(ne), 256, 0, s>>>(key2, idx2, w, ne, keep, err);
+    cudaMemcpyAsync(err_host, err, 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (*err_host != ~0ull) {
+        cudaMemcpy(err_key, key2 + (*err_host >> 1), 8, cudaMemcpyDeviceToHost);
+    } else {
+        // compact the run starts (keys, then value indices)
+        cub::DeviceSelect::Flagged(tmp, tk, key2, keep, key, nsel, (int)ne, s);
+        cub::DeviceSelect::Flagged(tmp, ti, idx2, keep, idx, nsel, (int)ne, s);
+        int cnt = 0;
+        cudaMemcpyAsync(&cnt, nsel, 4, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        *m = (uint64_t)cnt;
+        cudaMalloc(r_out, (cnt ? cnt : 1) * 4);
+        cudaMalloc(c_out, (cnt ? cnt : 1) * 4);
+        cudaMalloc(w_out, (cnt ? cnt : 1) * 8);
+        if (cnt) fold_unpack_kernel<<<blocks(cnt), 256, 0, s>>>(key, idx, w, cnt, *r_out, *c_out, *w_out);
+        cudaStreamSynchronize(s);
+    }
+    cudaFree(tmp); cudaFree(key); cudaFree(key2); cudaFree(idx); cudaFree(idx2);
+    cudaFree(keep); cudaFree(err); cudaFree(nsel);
+}
 
 // Device arrays r, c, w (ne entries) -> row_ptr (n+1, u64), col (nnz), val
 // (nnz), diag (n).  Scratch is allocated here.  Returns 0 on success, or the

@@ -17,19 +17,16 @@
 #include <unordered_set>
 #include <vector>
 
-#include "expmc_b200.h"
+#include "host_io.h"
 
-struct expmc_csr {
-    uint64_t n = 0;
-    std::vector<uint64_t> row_ptr;
-    std::vector<uint32_t> col;
-    std::vector<double> val;
-    std::vector<double> diag;
-};
+namespace expmc_b200 {
+std::string& host_error() {
+    thread_local std::string msg;
+    return msg;
+}
+}  // namespace expmc_b200
 
 namespace {
-
-thread_local std::string g_gen_err;
 
 // PCG32 RngStream, proj/include/expmc/rng.hpp:14-63
 struct Pcg {
@@ -59,16 +56,7 @@ struct Pcg {
 
 template <class F>
 int guarded(F&& f) {
-    try {
-        f();
-        return EXPMC_OK;
-    } catch (const std::invalid_argument& e) {
-        g_gen_err = e.what();
-        return EXPMC_INVALID_ARGUMENT;
-    } catch (const std::exception& e) {
-        g_gen_err = e.what();
-        return EXPMC_RUNTIME_ERROR;
-    }
+    return expmc_b200::host_guarded(f);
 }
 
 // Mirrored CSR from an undirected edge list (a != b, no duplicates),
@@ -100,7 +88,7 @@ expmc_csr* csr_from_edges(uint64_t n, const std::vector<uint32_t>& ea,
 
 extern "C" {
 
-const char* expmc_gen_last_error(void) { return g_gen_err.c_str(); }
+const char* expmc_gen_last_error(void) { return expmc_b200::host_error().c_str(); }
 
 int expmc_gen_fd(int dim, uint64_t side, double s, expmc_csr** out) {
     return guarded([&] {

@@ -83,6 +83,10 @@ void from_entries_device(uint64_t n, const uint32_t* r, const uint32_t* c, const
                          uint64_t ne, uint64_t* row_ptr, uint32_t** col_out, double** val_out,
                          double* diag, uint64_t* nnz_out, unsigned long long* err_host,
                          unsigned long long* dup_key, cudaStream_t s);
+void fold_general_device(const uint32_t* r, const uint32_t* c, const double* w, uint64_t ne,
+                         uint32_t** r_out, uint32_t** c_out, double** w_out, uint64_t* m,
+                         unsigned long long* err_host, unsigned long long* err_key,
+                         cudaStream_t s);
 
 // metrics.cu (§8f f4)
 bool rank_device(const double* scores_host, uint64_t n, uint32_t* order_host, cudaStream_t s);

@@ -16,6 +16,7 @@ parallelism; results do not depend on it).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 import math
 from dataclasses import dataclass, field
@@ -211,6 +212,19 @@ def from_entries(n: int, rows, cols, weights, device=0) -> SplitMatrix:
                                                c.ctypes.data_as(u32p), w.ctypes.data_as(f64p),
                                                len(w), int(device), C.byref(h)))
     return SplitMatrix(h, n)
+
+
+def from_matrix_market(path, device=0) -> SplitMatrix:
+    """load_matrix_market + split() (matrix_market.cpp:51-165,
+    sparse_matrix.cpp:101-142): host parse on all cores, general fold,
+    from_entries and split on the GPU.  Parse errors raise ExpmcError
+    ("path:line: what", the reference's runtime_error); from_entries errors
+    raise ValueError."""
+    h = C.c_void_p()
+    check(lib().expmc_cuda_create_from_mm(os.fsencode(path), int(device), C.byref(h)))
+    n = C.c_uint64()
+    check(lib().expmc_cuda_matrix_info(h, C.byref(n), None, None, None, None, None))
+    return SplitMatrix(h, n.value)
 
 
 def split(csr, device=0) -> SplitMatrix:

@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -80,6 +81,103 @@ def gen_row_sample(n: int, k: int, seed: int) -> np.ndarray:
     return out
 
 
+# ------------------------------------------- Matrix Market + CSR cache (f1, f3)
+@dataclass
+class MmEntries:
+    """One parsed Matrix Market file before the fold / from_entries."""
+    n: int
+    general: bool
+    pattern: bool
+    last_line: int
+    rows: np.ndarray   # uint32, 0-based, file order
+    cols: np.ndarray
+    weights: np.ndarray
+
+
+def parse_matrix_market(path) -> MmEntries:
+    """The parse half of load_matrix_market (matrix_market.cpp:51-131), on all
+    host cores.  Errors raise ExpmcError("path:line: what")."""
+    L = lib()
+    h = C.c_void_p()
+    check(L.expmc_mm_parse(os.fsencode(path), C.byref(h)), gen=True)
+    try:
+        n, ne, last = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        g, pt = C.c_int32(), C.c_int32()
+        check(L.expmc_mm_info(h, C.byref(n), C.byref(ne), C.byref(g), C.byref(pt), C.byref(last)),
+              gen=True)
+        r, c, w = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(L.expmc_mm_view(h, C.byref(r), C.byref(c), C.byref(w)), gen=True)
+        k = ne.value
+
+        def arr(p, t, dt):
+            if k == 0:
+                return np.zeros(0, dt)
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(t)), (k,)).astype(dt, copy=True)
+
+        return MmEntries(n.value, bool(g.value), bool(pt.value), last.value,
+                         arr(r, C.c_uint32, np.uint32), arr(c, C.c_uint32, np.uint32),
+                         arr(w, C.c_double, np.float64))
+    finally:
+        L.expmc_mm_free(h)
+
+
+def load_matrix_market(path, device=0) -> Csr:
+    """load_matrix_market (matrix_market.cpp:51-165) -> the SparseSymmetric
+    adjacency (fold + from_entries on the GPU)."""
+    h = C.c_void_p()
+    check(lib().expmc_cuda_mm_load(os.fsencode(path), int(device), C.byref(h)))
+    return _take(h)
+
+
+def _csr_args(csr: Csr):
+    rp = np.ascontiguousarray(csr.row_ptr, np.uint64)
+    col = np.ascontiguousarray(csr.col, np.uint32)
+    val = np.ascontiguousarray(csr.val, np.float64)
+    diag = np.ascontiguousarray(csr.diag, np.float64)
+    return (int(csr.n), rp.ctypes.data_as(u64p), col.ctypes.data_as(u32p),
+            val.ctypes.data_as(f64p), diag.ctypes.data_as(f64p)), (rp, col, val, diag)
+
+
+def write_matrix_market(csr: Csr, path) -> None:
+    """write_matrix_market (matrix_market.cpp:167-194): lower triangle,
+    1-based, ``pattern`` when every weight is 1, shortest round-trip reals."""
+    args, _keep = _csr_args(csr)
+    check(lib().expmc_mm_write(os.fsencode(path), *args), gen=True)
+
+
+def save_csr(csr: Csr, path) -> None:
+    """Binary CSR cache: header + arrays + checksum."""
+    args, _keep = _csr_args(csr)
+    check(lib().expmc_csr_save(os.fsencode(path), *args), gen=True)
+
+
+def load_csr(path) -> Csr:
+    """Read a binary CSR cache written by :func:`save_csr` (size, checksum and
+    row_ptr verified)."""
+    h = C.c_void_p()
+    check(lib().expmc_csr_load(os.fsencode(path), C.byref(h)), gen=True)
+    return _take(h)
+
+
+def _cached(name: str, make) -> Csr:
+    """Generated graph through the CSR cache in $EXPMC_CSR_CACHE (if set)."""
+    d = os.environ.get("EXPMC_CSR_CACHE")
+    if not d:
+        return make()
+    path = os.path.join(d, name + ".csr")
+    if os.path.exists(path):
+        try:
+            return load_csr(path)
+        except Exception:
+            pass  # stale / corrupt: regenerate
+    csr = make()
+    os.makedirs(d, exist_ok=True)
+    tmp = f"{path}.{os.getpid()}.tmp"
+    save_csr(csr, tmp)
+    os.replace(tmp, path)
+    return csr
+
+
 def csr_from_dense(a: np.ndarray) -> Csr:
     """Small symmetric dense matrix -> Csr (tests)."""
     a = np.asarray(a, dtype=np.float64)
@@ -138,7 +236,7 @@ def build_config(idx: int, scale: float = 1.0, lambda_max=None) -> Config:
         beta, W, rows, name = 1.0, 10_000, None, f"fd2d_{side}x{side}"
     elif idx == 2:
         n = max(1000, int(1e5 * scale))
-        csr = gen_ba(n, 5, 1)
+        csr = _cached(f"ba_n{n}_m5_s1", lambda: gen_ba(n, 5, 1))
         v = np.ones(n)
         if lambda_max is None:
             from .estimator import split as _split
@@ -147,7 +245,7 @@ def build_config(idx: int, scale: float = 1.0, lambda_max=None) -> Config:
         beta, W, rows, name = 0.5 / lambda_max, 10_000, None, f"ba_n{n}_m5"
     elif idx == 3:
         n = max(1000, int(1e6 * scale))
-        csr = gen_ws(n, 5, 0.1, 1)
+        csr = _cached(f"ws_n{n}_k5_p0.1_s1", lambda: gen_ws(n, 5, 0.1, 1))
         v = np.ones(n)
         beta, W, rows, name = 0.05, 2_000, None, f"ws_n{n}_k10_p0.1"
     elif idx == 4:
@@ -160,7 +258,7 @@ def build_config(idx: int, scale: float = 1.0, lambda_max=None) -> Config:
         beta, W, name = 1e-4, 10_000, f"fd3d_{side}^3"
     elif idx == 5:
         n = max(1000, int(1e7 * scale))
-        csr = gen_ba(n, 8, 1)
+        csr = _cached(f"ba_n{n}_m8_s1", lambda: gen_ba(n, 8, 1))
         v = gen_vector(1, n, 2)
         beta, W, rows, name = 0.02, 1_000, None, f"ba_n{n}_m8"
     else:

@@ -11,8 +11,9 @@ these are produced from the compiled reference itself:
   advance.json  advance() end states / jumps per stream   sampler.cpp:36-49
   ba.json       generate({ScaleFree, ...}) CSR            generators.cpp:58-103
   philox.json   Philox4x32-10 known answers (curand)
+  mm.json       load/write_matrix_market outcomes       matrix_market.cpp:51-207
 
-usage: python tests/golden/make_golden.py    (needs /root/reference + nvcc)
+usage: python tests/golden/make_golden.py [mm]   (needs /root/reference + nvcc)
 """
 import json
 import os
@@ -181,5 +182,45 @@ int main() {
     print("golden fixtures written to", HERE)
 
 
+def mm_goldens():
+    """mm.json: load_matrix_market outcomes for tests/mm_cases.py and
+    write_matrix_market texts, from the reference (matrix_market.cpp)."""
+    sys.path.insert(0, os.path.dirname(HERE))
+    from mm_cases import CASES
+
+    def csr_json(rm):
+        s = rm.split()
+        return {"n": rm.n, "row_offset": [int(x) for x in s["row_offset"]],
+                "neighbor": [int(x) for x in s["neighbor"]], "weight": fl(s["weight"]),
+                "diag": fl(s["diag"])}
+
+    cases, writes = [], []
+    with tempfile.TemporaryDirectory() as d:
+        for name, body in CASES:
+            p = os.path.join(d, name + ".mtx")
+            with open(p, "w", newline="") as f:
+                f.write(body)
+            try:
+                out = {"ok": True, **csr_json(ref.mm_load(p))}
+            except oracle.RefError as e:
+                out = {"ok": False, "kind": e.kind, "message": str(e).replace(p, "{path}")}
+            cases.append({"name": name, "body": body, **out})
+        mats = small_matrices()
+        mats["awkward_reals"] = (6, [0, 0, 1, 2, 3, 4, 5], [1, 2, 3, 4, 5, 5, 0],
+                                 [0.1, 1.0 / 3.0, 1e-300, 1e300, 5e-324, 123456789.125, 7.0])
+        for name, (n, r, c, w) in sorted(mats.items()):
+            rm = ref.matrix_from_entries(n, r, c, w)
+            p = os.path.join(d, name + ".out.mtx")
+            ref.mm_write_entries(n, r, c, w, p)
+            with open(p) as f:
+                writes.append({"name": name, **csr_json(rm), "text": f.read()})
+    dump("mm.json", {"source": "reference load/write_matrix_market (oracle/_ref)",
+                     "cases": cases, "writes": writes})
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["mm"]:
+        mm_goldens()
+    else:
+        main()
+        mm_goldens()

@@ -17,7 +17,7 @@ GOLD = os.path.join(ROOT, "tests", "golden")
 
 def test_library_exports_every_header_symbol(pb):
     hdr = open(os.path.join(ROOT, "include", "expmc_b200.h")).read()
-    names = sorted(set(re.findall(r"\b(expmc_(?:cuda|gen|csr)_\w+)\s*\(", hdr)))
+    names = sorted(set(re.findall(r"\b(expmc_(?:cuda|gen|csr|mm)_\w+)\s*\(", hdr)))
     assert len(names) >= 25
     L = pb.lib()
     missing = [n for n in names if not hasattr(L, n)]
