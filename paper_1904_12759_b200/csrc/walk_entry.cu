@@ -58,32 +58,35 @@ constexpr unsigned FULL = 0xffffffffu;
 #define ENTRY_POP_MIN 2 // run the scheduler once this many lanes are idle
 #endif
 
-struct RowConst {    // per task: the start row and its constants
-    uint32_t i;      // matrix row            (i, chunk adjacent: one LDS.64)
+struct RowConst {    // per task: the start row and its constants (9 words used)
+    RowRec rr;       // record of the row                          words 0-3
+    uint32_t i;      // matrix row                                 word 4
     uint32_t chunk;  // chunk index (ChunkMeta only)
-    unsigned long long T0;  // never-jump threshold on a u32 draw
-    RowRec rr;       // record of the row
+    uint32_t T0;     // never-jump threshold on a u32 draw          word 5
+    uint32_t dead;   // 1: e^{-rate β} rounds to 1, no walker ever jumps
     double f0;       // e^{β d_i} v_i (score of a walker that never jumps)
     double K;        // shift of the deviation sums: f0 when never-jumpers are the
                      // majority (T0 >= 2^31), else 0 (no cancellation against a
                      // huge f0 that no walker realises, e.g. BA hubs)
     double corr;     // weight correction at the start state (½ d_i Strang, d_i Lie)
 };
+constexpr int kRowWords = 9;
 
 struct ChunkMeta {
-    RowConst row;           // row.chunk = chunk index within the row
-    uint32_t tstart, tend;  // the chunk's ticket range (counters)
-    uint32_t task;          // task id
+    RowConst row;           // row.chunk = chunk index within the row   words 0-11
+    uint32_t tstart, tend;  // the chunk's ticket range (counters)       word 12
+    uint32_t task;          // task id                                   word 13
     uint32_t last;          // last chunk of its task
-    uint32_t jm[4];         // jumper bitmask of slots 32q + lane (sweep ballots)
+    uint32_t jm[4];         // jumper bitmask of slots 32q + lane          words 14-15
 };
+static_assert(sizeof(RowConst) == 96 && sizeof(ChunkMeta) == 128, "meta layout");
 
 template <int R, int CAP>
 struct WarpState {
     double S[CAP];      // per ticket: raw weight sum at finish, then f - f0
     double v[CAP];      // per ticket: v at the end state
-    uint32_t w[CAP];    // per ticket: decision word until started, then jump count
-    uint16_t rs[CAP];   // per ticket: ring slot << 8 | chunk slot
+    uint2 tk[CAP];      // per ticket: {decision word until started, then jump
+                        //   count; ring slot << 8 | chunk slot}
     double dev[kChunk]; // finalize scatter buffer (slot order)
     ChunkMeta meta[R];
     RowConst adm;       // row of the task being admitted
@@ -124,11 +127,13 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             const uint32_t i = rows[t / WPR];
             const RowRec ri = load_rec(rec, i);
             const double p0 = exp_det(-__dmul_rn(__ldg(rate + i), p.beta));
+            const unsigned long long T0 = (unsigned long long)__dmul_rn(p0, 4294967296.0);
             a.rr = ri;
             a.i = i;
-            a.T0 = (unsigned long long)__dmul_rn(p0, 4294967296.0);
+            a.T0 = (uint32_t)T0;
+            a.dead = T0 >> 32 ? 1u : 0u;  // T0 = 2^32: never jumps
             a.f0 = __dmul_rn(exp_det(__dmul_rn(p.beta, ri.d)), ri.v);
-            a.K = a.T0 >= (1ull << 31) ? a.f0 : 0.0;
+            a.K = T0 >= (1ull << 31) ? a.f0 : 0.0;
             a.corr = p.strang ? __dmul_rn(0.5, ri.d) : ri.d;
         }
         __syncwarp();
@@ -137,6 +142,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
 
     int oldest = 0, live = 0;
     uint32_t head = 0, tail = 0;  // ticket counters (positions mod CAP)
+    uint32_t tbase = 0;           // first ticket of the oldest live chunk (= tail if none)
     // lane-private walker state
     bool act = false;
     uint32_t tk = 0, rsl = 0, off = 0, degf = 0, G = 0, jc = 0, ew = 0;
@@ -159,7 +165,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             const uint32_t pos = tk & (CAP - 1);
             q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, dcur)) : S;
             q.v[pos] = vcur;
-            q.w[pos] = jc;
+            q.tk[pos].x = jc;
             act = false;
             fin = true;
         } else {
@@ -183,10 +189,13 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             // ---- admit: sweep chunks while queued tickets cannot feed the
             // idle lanes and a whole chunk's tickets fit in the ring
             while (live < R && atask < ntask && tail - head < (uint32_t)__popc(idle) &&
-                   tail + kChunk - (live ? q.meta[oldest].tstart : tail) <= CAP) {
+                   tail + kChunk - tbase <= CAP) {
                 const int rs = (oldest + live) & (R - 1);
                 const uint32_t base = achunk * kChunk;
-                const uint64_t T0 = q.adm.T0;
+                const uint64_t rem = p.W - base;
+                const uint32_t nw = rem < (uint64_t)kChunk ? (uint32_t)rem : (uint32_t)kChunk;
+                const uint32_t lim = q.adm.dead ? 0u : nw;  // walkers that may jump
+                const uint32_t T0 = q.adm.T0;
                 const U4 D = philox4x32_10(
                     U4{0xffffffffu, base + (uint32_t)lane, q.adm.i, kTagEntry}, p.rk);
                 const uint32_t wd[4] = {D.x, D.y, D.z, D.w};
@@ -195,27 +204,25 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
                     const uint32_t sl = 32u * qq + lane;
-                    const bool jmp = (uint64_t)(base + sl) < p.W && (uint64_t)wd[qq] >= T0;
+                    const bool jmp = sl < lim && wd[qq] >= T0;
                     const unsigned b = __ballot_sync(FULL, jmp);
                     bq[qq] = b;
-                    if (jmp) {
-                        const uint32_t pos = (tail + __popc(b & lt)) & (CAP - 1);
-                        q.w[pos] = wd[qq];
-                        q.rs[pos] = (uint16_t)((rs << 8) | sl);
-                    }
+                    if (jmp) q.tk[(tail + __popc(b & lt)) & (CAP - 1)] =
+                                 make_uint2(wd[qq], ((uint32_t)rs << 8) | sl);
                     tail += __popc(b);
                 }
                 const uint32_t nextc = achunk + WPR;
-                if (lane == 0) {
-                    ChunkMeta& m = q.meta[rs];
-                    m.row = q.adm;
-                    m.row.chunk = achunk;
-                    m.tstart = t0;
-                    m.tend = tail;
-                    m.task = atask;
-                    m.last = nextc >= nch;
-#pragma unroll
-                    for (int qq = 0; qq < 4; ++qq) m.jm[qq] = bq[qq];
+                {   // chunk meta: one 8-byte word per lane
+                    uint64_t* dst = reinterpret_cast<uint64_t*>(&q.meta[rs]);
+                    const uint64_t* src = reinterpret_cast<const uint64_t*>(&q.adm);
+                    uint64_t x = 0;
+                    if (lane < kRowWords) x = src[lane];
+                    if (lane == 4) x = (x & 0xffffffffull) | ((uint64_t)achunk << 32);
+                    if (lane == 12) x = t0 | ((uint64_t)tail << 32);
+                    if (lane == 13) x = atask | ((uint64_t)(nextc >= nch) << 32);
+                    if (lane == 14) x = bq[0] | ((uint64_t)bq[1] << 32);
+                    if (lane == 15) x = bq[2] | ((uint64_t)bq[3] << 32);
+                    if (lane < kRowWords || (lane >= 12 && lane < 16)) dst[lane] = x;
                 }
                 __syncwarp();
                 ++live;
@@ -233,12 +240,12 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             const uint32_t rank = (uint32_t)__popc(idle & lt);
             if (!act && rank < take) {
                 tk = head + rank;
-                const uint32_t pos = tk & (CAP - 1);
-                rsl = q.rs[pos];
+                const uint2 t2 = q.tk[tk & (CAP - 1)];
+                rsl = t2.y;
+                ew = t2.x;
                 const ChunkMeta& m = q.meta[rsl >> 8];
                 off = m.row.rr.off; degf = m.row.rr.deg_flags;
                 ir = m.row.rr.inv_rate; dcur = m.row.rr.d; vcur = m.row.rr.v;
-                ew = q.w[pos];
                 t = 0.0; S = 0.0; G = 0; jc = 0;
                 act = true;
                 // a jumper's first sojourn ends in a jump (decision word >= T0),
@@ -282,20 +289,23 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         // ticket or retired a walker)
         if (!(idle | __ballot_sync(FULL, fin))) continue;
         __syncwarp();
+        // oldest ticket still walking, as an offset from tbase (~0: none);
+        // a chunk is done once all its tickets are popped and none walks
+        const uint32_t base0 = tbase;
+        const uint32_t minoff = __reduce_min_sync(FULL, act ? tk - base0 : ~0u);
         while (live > 0) {
             const ChunkMeta& m = q.meta[oldest];
             const uint32_t ts = m.tstart, te = m.tend;
-            if ((int)(head - te) < 0 ||
-                __ballot_sync(FULL, act && tk - ts < te - ts) != 0)
-                break;
+            if ((int)(head - te) < 0 || te - base0 > minoff) break;
             const double f0 = m.row.f0, K = m.row.K, corr = m.row.corr;
             const uint64_t base = (uint64_t)m.row.chunk * kChunk;
             unsigned long long jl = 0;
             for (uint32_t k = ts + lane; k < te; k += 32) {
                 const uint32_t pos = k & (CAP - 1);
                 const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], corr));
-                q.dev[q.rs[pos] & 255u] = __dsub_rn(__dmul_rn(exp_det(x), q.v[pos]), K);
-                jl += q.w[pos];
+                const uint2 t2 = q.tk[pos];
+                q.dev[t2.y & 255u] = __dsub_rn(__dmul_rn(exp_det(x), q.v[pos]), K);
+                jl += t2.x;
             }
             __syncwarp();
 #pragma unroll
@@ -311,6 +321,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             jsum += jl;
             njt += te - ts;
             nwt += (uint32_t)(p.W - base < (uint64_t)kChunk ? p.W - base : (uint64_t)kChunk);
+            tbase = te;  // the next chunk's tickets start where this one's end
             if (m.last) {
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
