@@ -34,7 +34,9 @@
 //    l ≡ s (mod 32) with floor(l/128) ≡ w (mod WPR) in increasing l; lanes are
 //    combined by an xor butterfly, parts in index order.  Independent of
 //    scheduling, grid shape, GPU count and row sharding.
+#include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -54,12 +56,25 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef ENTRY_CAP
 #define ENTRY_CAP 256   // jumper tickets in flight per warp (power of 2, >= 128)
 #endif
+#ifndef ENTRY_PREFETCH
+#define ENTRY_PREFETCH 0  // tickets kept queued after each jump (0: off; 16-64 measured 2-3% slower)
+#endif
+#ifndef ENTRY_CARVE
+#define ENTRY_CARVE 1     // size the smem carveout for ENTRY_MIN_BLOCKS (max L1)
+#endif
 #ifndef ENTRY_POP_MIN
 #define ENTRY_POP_MIN 2 // run the scheduler once this many lanes are idle
 #endif
 
-struct RowConst {    // per task: the start row and its constants (9 words used)
-    RowRec rr;       // record of the row                          words 0-3
+struct RowRecU {     // RowRec without its 32-byte alignment (smem copy)
+    uint32_t off, deg_flags;
+    float inv_rate;
+    uint32_t spare;
+    double d, v;
+};
+
+struct RowConst {    // per task: the start row and its constants (9 words)
+    RowRecU rr;      // record of the row                          words 0-3
     uint32_t i;      // matrix row                                 word 4
     uint32_t chunk;  // chunk index (ChunkMeta only)
     uint32_t T0;     // never-jump threshold on a u32 draw          word 5
@@ -73,17 +88,17 @@ struct RowConst {    // per task: the start row and its constants (9 words used)
 constexpr int kRowWords = 9;
 
 struct ChunkMeta {
-    RowConst row;           // row.chunk = chunk index within the row   words 0-11
-    uint32_t tstart, tend;  // the chunk's ticket range (counters)       word 12
-    uint32_t task;          // task id                                   word 13
+    RowConst row;           // row.chunk = chunk index within the row   words 0-8
+    uint32_t tstart, tend;  // the chunk's ticket range (counters)       word 9
+    uint32_t task;          // task id                                   word 10
     uint32_t last;          // last chunk of its task
-    uint32_t jm[4];         // jumper bitmask of slots 32q + lane          words 14-15
+    uint32_t jm[4];         // jumper bitmask of slots 32q + lane          words 11-12
 };
-static_assert(sizeof(RowConst) == 96 && sizeof(ChunkMeta) == 128, "meta layout");
+static_assert(sizeof(RowConst) == 8 * kRowWords && sizeof(ChunkMeta) == 104, "meta layout");
 
 template <int R, int CAP>
 struct WarpState {
-    double S[CAP];      // per ticket: raw weight sum at finish, then f - f0
+    double S[CAP];      // per ticket: raw weight sum at finish
     double v[CAP];      // per ticket: v at the end state
     uint2 tk[CAP];      // per ticket: {decision word until started, then jump
                         //   count; ring slot << 8 | chunk slot}
@@ -128,7 +143,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             const RowRec ri = load_rec(rec, i);
             const double p0 = exp_det(-__dmul_rn(__ldg(rate + i), p.beta));
             const unsigned long long T0 = (unsigned long long)__dmul_rn(p0, 4294967296.0);
-            a.rr = ri;
+            a.rr = RowRecU{ri.off, ri.deg_flags, ri.inv_rate, 0u, ri.d, ri.v};
             a.i = i;
             a.T0 = (uint32_t)T0;
             a.dead = T0 >> 32 ? 1u : 0u;  // T0 = 2^32: never jumps
@@ -177,6 +192,56 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         }
     };
 
+    // Sweep the next chunk of the admission task: decide its walkers and
+    // append the jumpers as tickets (ring slot rs = next meta slot).
+    auto can_admit = [&] {
+        return live < R && atask < ntask && tail + kChunk - tbase <= CAP;
+    };
+    auto admit_chunk = [&] {
+        const int rs = (oldest + live) & (R - 1);
+        const uint32_t base = achunk * kChunk;
+        const uint64_t rem = p.W - base;
+        const uint32_t nw = rem < (uint64_t)kChunk ? (uint32_t)rem : (uint32_t)kChunk;
+        const uint32_t lim = q.adm.dead ? 0u : nw;  // walkers that may jump
+        const uint32_t T0 = q.adm.T0;
+        const U4 D = philox4x32_10(
+            U4{0xffffffffu, base + (uint32_t)lane, q.adm.i, kTagEntry}, p.rk);
+        const uint32_t wd[4] = {D.x, D.y, D.z, D.w};
+        const uint32_t t0 = tail;
+        unsigned bq[4];
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+            const uint32_t sl = 32u * qq + lane;
+            const bool jmp = sl < lim && wd[qq] >= T0;
+            const unsigned b = __ballot_sync(FULL, jmp);
+            bq[qq] = b;
+            if (jmp) q.tk[(tail + __popc(b & lt)) & (CAP - 1)] =
+                         make_uint2(wd[qq], ((uint32_t)rs << 8) | sl);
+            tail += __popc(b);
+        }
+        const uint32_t nextc = achunk + WPR;
+        {   // chunk meta: one 8-byte word per lane
+            uint64_t* dst = reinterpret_cast<uint64_t*>(&q.meta[rs]);
+            const uint64_t* src = reinterpret_cast<const uint64_t*>(&q.adm);
+            uint64_t x = 0;
+            if (lane < kRowWords) x = src[lane];
+            if (lane == 4) x = (x & 0xffffffffull) | ((uint64_t)achunk << 32);
+            if (lane == 9) x = t0 | ((uint64_t)tail << 32);
+            if (lane == 10) x = atask | ((uint64_t)(nextc >= nch) << 32);
+            if (lane == 11) x = bq[0] | ((uint64_t)bq[1] << 32);
+            if (lane == 12) x = bq[2] | ((uint64_t)bq[3] << 32);
+            if (lane < 13) dst[lane] = x;
+        }
+        __syncwarp();
+        ++live;
+        if (nextc < nch) {
+            achunk = nextc;
+        } else {
+            atask += tstride;
+            if (atask < ntask) load_task(atask);
+        }
+    };
+
     while (true) {
         // ---- A: sojourn of every walker in flight
         bool fin = false, jmp = false;
@@ -188,51 +253,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         if (idle) {
             // ---- admit: sweep chunks while queued tickets cannot feed the
             // idle lanes and a whole chunk's tickets fit in the ring
-            while (live < R && atask < ntask && tail - head < (uint32_t)__popc(idle) &&
-                   tail + kChunk - tbase <= CAP) {
-                const int rs = (oldest + live) & (R - 1);
-                const uint32_t base = achunk * kChunk;
-                const uint64_t rem = p.W - base;
-                const uint32_t nw = rem < (uint64_t)kChunk ? (uint32_t)rem : (uint32_t)kChunk;
-                const uint32_t lim = q.adm.dead ? 0u : nw;  // walkers that may jump
-                const uint32_t T0 = q.adm.T0;
-                const U4 D = philox4x32_10(
-                    U4{0xffffffffu, base + (uint32_t)lane, q.adm.i, kTagEntry}, p.rk);
-                const uint32_t wd[4] = {D.x, D.y, D.z, D.w};
-                const uint32_t t0 = tail;
-                unsigned bq[4];
-#pragma unroll
-                for (int qq = 0; qq < 4; ++qq) {
-                    const uint32_t sl = 32u * qq + lane;
-                    const bool jmp = sl < lim && wd[qq] >= T0;
-                    const unsigned b = __ballot_sync(FULL, jmp);
-                    bq[qq] = b;
-                    if (jmp) q.tk[(tail + __popc(b & lt)) & (CAP - 1)] =
-                                 make_uint2(wd[qq], ((uint32_t)rs << 8) | sl);
-                    tail += __popc(b);
-                }
-                const uint32_t nextc = achunk + WPR;
-                {   // chunk meta: one 8-byte word per lane
-                    uint64_t* dst = reinterpret_cast<uint64_t*>(&q.meta[rs]);
-                    const uint64_t* src = reinterpret_cast<const uint64_t*>(&q.adm);
-                    uint64_t x = 0;
-                    if (lane < kRowWords) x = src[lane];
-                    if (lane == 4) x = (x & 0xffffffffull) | ((uint64_t)achunk << 32);
-                    if (lane == 12) x = t0 | ((uint64_t)tail << 32);
-                    if (lane == 13) x = atask | ((uint64_t)(nextc >= nch) << 32);
-                    if (lane == 14) x = bq[0] | ((uint64_t)bq[1] << 32);
-                    if (lane == 15) x = bq[2] | ((uint64_t)bq[3] << 32);
-                    if (lane < kRowWords || (lane >= 12 && lane < 16)) dst[lane] = x;
-                }
-                __syncwarp();
-                ++live;
-                if (nextc < nch) {
-                    achunk = nextc;
-                } else {
-                    atask += tstride;
-                    if (atask < ntask) load_task(atask);
-                }
-            }
+            while (can_admit() && tail - head < (uint32_t)__popc(idle)) admit_chunk();
             // ---- pop: idle lanes take tickets in order
             const uint32_t avail = tail - head;
             const uint32_t nidle = (uint32_t)__popc(idle);
@@ -284,6 +305,11 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             ++jc;
             off = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d; vcur = e.v;
         }
+#if ENTRY_PREFETCH
+        // ---- refill the ring while this iteration's gathers are in flight
+        // (the pops before the next jump then rarely have to sweep)
+        while (can_admit() && tail - head < (uint32_t)ENTRY_PREFETCH) admit_chunk();
+#endif
         // ---- finalize the oldest chunks once all their walkers are done
         // (the condition can only change in an iteration that popped a
         // ticket or retired a walker)
@@ -404,11 +430,58 @@ __global__ void combine_parts_kernel(const double4* __restrict__ partial, uint64
 template <int WPR>
 int launch_t(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const FastParams& p,
              double* value, double* se, uint64_t* jumps, double4* partial, cudaStream_t s) {
+    // Exactly ENTRY_MIN_BLOCKS resident blocks per SM with the smallest
+    // shared-memory carveout that holds them, so the rest of the SM's 256 KB
+    // is L1 for the edge gathers.  The driver sizes the carveout for the
+    // maximum occupancy, which the register count alone would put at 7
+    // blocks (228 KB carveout, ~28 KB L1: measured 1.8x slower on the
+    // L1-local config 4); padding each block with dynamic shared memory so
+    // that a 7th block cannot fit pins 6 blocks at a 196 KB carveout.
+    // Grid = one wave of resident blocks (the kernel strides over tasks).
+    static int nsm = 0, pad = 0;
+    if (!nsm) {
+        int dev = 0, smem_sm = 0;
+        cudaFuncAttributes fa;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            nsm = 148;
+        int pct = -1;
+        if (ENTRY_CARVE && cudaFuncGetAttributes(&fa, entry_walk_kernel<WPR>) == cudaSuccess &&
+            cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) ==
+                cudaSuccess &&
+            smem_sm > 0) {
+            constexpr int B = ENTRY_MIN_BLOCKS, kReserve = 1024;
+            const long st = (long)fa.sharedSizeBytes;
+            const int kb[] = {0, 8, 16, 32, 64, 100, 132, 164, 196, 228};
+            long cap = smem_sm;
+            for (int c : kb)
+                if (c * 1024L >= B * (st + kReserve) && c * 1024L <= smem_sm) {
+                    cap = c * 1024L;
+                    break;
+                }
+            const long tmin = smem_sm / (B + 1) - kReserve + 1;  // B+1 blocks must not fit
+            const long tmax = cap / B - kReserve;                 // B blocks must fit in cap
+            if (tmin <= tmax) pad = (int)(tmin > st ? tmin - st : 0);
+            if (pad) cudaFuncSetAttribute(entry_walk_kernel<WPR>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+            // the driver rounds the percentage UP to a supported capacity
+            pct = (int)floor(100.0 * cap / smem_sm);
+            cudaFuncSetAttribute(entry_walk_kernel<WPR>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+        }
+        int resident = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, entry_walk_kernel<WPR>, 128, pad);
+        cudaGetLastError();
+        if (getenv("EXPMC_DEBUG"))
+            fprintf(stderr,
+                    "entry_walk_kernel<%d>: %d SMs, occupancy %d blocks/SM, pad %d B, carveout %d%%\n",
+                    WPR, nsm, resident, pad, pct);
+    }
     const uint64_t warps = nrows * WPR;
     const uint64_t blocks = (warps + 3) / 4;
-    const uint64_t cap = 148ull * ENTRY_MIN_BLOCKS;  // one wave of resident blocks
+    const uint64_t cap = (uint64_t)nsm * ENTRY_MIN_BLOCKS;
     const unsigned grid = (unsigned)(blocks < cap ? blocks : cap);
-    entry_walk_kernel<WPR><<<grid, 128, 0, s>>>(m.rec, m.rate, m.adj, m.alias_thr, m.alias_idx,
+    entry_walk_kernel<WPR><<<grid, 128, pad, s>>>(m.rec, m.rate, m.adj, m.alias_thr, m.alias_idx,
                                                 rows, nrows, p, value, se, jumps, partial);
     if (WPR > 1) {
         combine_parts_kernel<WPR><<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(
