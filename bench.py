@@ -462,7 +462,7 @@ def e2e(pb, m, cfg, rows, args, K, Wm):
         p = pb.PathParams(cfg.beta, cfg.n_steps, cfg.walkers, pb.Splitting.Strang,
                           args.seed + k, pb.Rng.PHILOX)
         r = pb.entries_estimate(m, v_h, rows_h, p, out=outs)
-        return int(r.jumps[:nrows].sum())
+        return r.total_jumps
 
     for k in range(Wm):
         call(k)

@@ -115,10 +115,12 @@ int expmc_cuda_records_export(const expmc_matrix* m, void* out);
 int expmc_cuda_entry_estimate(expmc_matrix* m, const double* v, uint64_t nv, uint32_t i,
                               const expmc_path_params* p, expmc_estimate* out);
 /* Batched entry_estimate over rows[0..nrows) (rows == NULL: every row,
- * nrows must equal n): the "full vector with W walkers per entry". */
+ * nrows must equal n): the "full vector with W walkers per entry".
+ * total_jumps (may be NULL) receives the sum of jumps[] (reduced on the
+ * device for the Philox walker). */
 int expmc_cuda_entries(expmc_matrix* m, const double* v, uint64_t nv, const uint32_t* rows,
                        uint64_t nrows, const expmc_path_params* p, double* value,
-                       double* std_error, uint64_t* jumps);
+                       double* std_error, uint64_t* jumps, uint64_t* total_jumps);
 /* vector_estimate (estimator.cpp:208-278), Theorem 2; values has n entries. */
 int expmc_cuda_vector_estimate(expmc_matrix* m, const double* v, uint64_t nv,
                                const expmc_path_params* p, double* values,

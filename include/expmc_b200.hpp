@@ -61,6 +61,7 @@ struct VectorEstimate {
 struct EntriesEstimate {
     std::vector<double> values, std_errors;
     std::vector<std::uint64_t> jumps;
+    std::uint64_t total_jumps = 0;
 };
 
 inline void check(int rc) {
@@ -129,7 +130,8 @@ inline EntriesEstimate entries_estimate(const SplitMatrix& m, std::span<const do
     EntriesEstimate out{std::vector<double>(k), std::vector<double>(k),
                         std::vector<std::uint64_t>(k)};
     check(expmc_cuda_entries(m.handle(), v.data(), v.size(), rows.empty() ? nullptr : rows.data(),
-                             k, &c, out.values.data(), out.std_errors.data(), out.jumps.data()));
+                             k, &c, out.values.data(), out.std_errors.data(), out.jumps.data(),
+                             &out.total_jumps));
     return out;
 }
 

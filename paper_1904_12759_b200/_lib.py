@@ -53,7 +53,7 @@ SIGNATURES = [
     ("expmc_cuda_entry_estimate", C.c_int,
      [vp, f64p, C.c_uint64, C.c_uint32, C.POINTER(PathParamsC), C.POINTER(EstimateC)]),
     ("expmc_cuda_entries", C.c_int,
-     [vp, f64p, C.c_uint64, u32p, C.c_uint64, C.POINTER(PathParamsC), f64p, f64p, u64p]),
+     [vp, f64p, C.c_uint64, u32p, C.c_uint64, C.POINTER(PathParamsC), f64p, f64p, u64p, u64p]),
     ("expmc_cuda_vector_estimate", C.c_int,
      [vp, f64p, C.c_uint64, C.POINTER(PathParamsC), f64p, f64p, u64p, f64p]),
     ("expmc_cuda_tc_estimate", C.c_int, [vp, C.POINTER(PathParamsC), C.POINTER(EstimateC)]),

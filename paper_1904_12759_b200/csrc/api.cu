@@ -7,7 +7,10 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -453,7 +456,7 @@ void upload_and_convert(uint64_t n, const uint32_t* rows, const uint32_t* cols, 
 // Run the entry estimator for host rows / host v; outputs to host.
 void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* rows,
                  uint64_t nrows, const expmc_path_params* p, double* value, double* se,
-                 uint64_t* jumps) {
+                 uint64_t* jumps, uint64_t* total_jumps = nullptr) {
     validate_params(p);
     const bool fast = p->rng == EXPMC_RNG_PHILOX;
     if (fast) {
@@ -475,18 +478,37 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
     if (nrows == 0) return;
     DeviceGuard g(h->device);
     cudaStream_t s = h->stream;
+    // EXPMC_DEBUG=2: per-stage device timeline of the call on stderr
+    static const bool trace = [] {
+        const char* e = getenv("EXPMC_DEBUG");
+        return e && atoi(e) >= 2;
+    }();
+    cudaEvent_t ev[16];
+    int nev = 0;
+    auto mark = [&](cudaStream_t st) {
+        if (!trace || nev >= 16) return;
+        cudaEventCreate(&ev[nev]);
+        cudaEventRecord(ev[nev++], st);
+    };
+    const auto t_host0 = std::chrono::steady_clock::now();
+    mark(s);
     double* vd = h->vdev.get<double>(n);
     CK(cudaMemcpyAsync(vd, v, n * 8, cudaMemcpyHostToDevice, s));
+    mark(s);
     if (fast) {
         // E2E path: device finiteness check, then the rows in pieces whose
         // results are copied back on a second stream while the next piece
-        // runs (the walker work of different rows is independent)
-        unsigned int* flag = h->scal.get<unsigned int>(4);
-        CK(cudaMemsetAsync(flag, 0, 4, s));
+        // runs (the walker work of different rows is independent).
+        // scal: [0] non-finite flag (u32), [1] total jumps (u64)
+        unsigned long long* sc = h->scal.get<unsigned long long>(4);
+        unsigned int* flag = reinterpret_cast<unsigned int*>(sc);
+        unsigned long long* jtot = sc + 1;
+        CK(cudaMemsetAsync(sc, 0, 16, s));
         launch_count_nonfinite(n, vd, flag, s);
         launch_pack_v(n, vd, h->m.rec, s);
         launch_pack_v_adj(h->m.nnz, vd, h->m.adj, s);
         after_launch(3);
+        mark(s);
         if (nrows >= (1ull << 30)) throw InvalidArg("at most 2^30 rows per call");
         const uint32_t* rd;
         if (rows) {
@@ -499,16 +521,26 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
         double* ov = h->out_val.get<double>(nrows);
         double* os = h->out_se.get<double>(nrows);
         uint64_t* oj = h->out_j.get<uint64_t>(nrows);
-        const uint64_t pieces = nrows >= (1ull << 20) ? 4 : 1;
+        static const int env_pieces = [] {
+            const char* e = getenv("EXPMC_PIECES");  // experiments only
+            return e ? atoi(e) : 0;
+        }();
+        const uint64_t pieces = env_pieces > 0 ? (uint64_t)env_pieces
+                                               : (nrows >= (1ull << 20) ? 8 : 1);
         void* scratch =
             h->part.get<unsigned char>(entry_fast_scratch_bytes((nrows + pieces - 1) / pieces,
                                                                 p->samples));
         const FastParams fp = fast_params(p, p->samples);
         for (uint64_t k = 0; k < pieces; ++k) {
             const uint64_t lo = nrows * k / pieces, hi = nrows * (k + 1) / pieces;
-            const int kl = launch_entry_fast(h->m, rd + lo, hi - lo, fp, ov + lo, os + lo, oj + lo,
+            int kl = launch_entry_fast(h->m, rd + lo, hi - lo, fp, ov + lo, os + lo, oj + lo,
                                              scratch, s);
+            if (total_jumps) {
+                launch_sum_u64(hi - lo, oj + lo, jtot, s);
+                ++kl;
+            }
             after_launch(kl);
+            mark(s);
             CK(cudaEventRecord(h->piece_done, s));
             CK(cudaStreamWaitEvent(h->copy_stream, h->piece_done, 0));
             CK(cudaMemcpyAsync(value + lo, ov + lo, (hi - lo) * 8, cudaMemcpyDeviceToHost,
@@ -518,11 +550,25 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
             CK(cudaMemcpyAsync(jumps + lo, oj + lo, (hi - lo) * 8, cudaMemcpyDeviceToHost,
                                h->copy_stream));
         }
-        unsigned int bad = 0;
-        CK(cudaMemcpyAsync(&bad, flag, 4, cudaMemcpyDeviceToHost, s));
+        unsigned long long res[2] = {0, 0};
+        CK(cudaMemcpyAsync(res, sc, 16, cudaMemcpyDeviceToHost, s));
+        mark(h->copy_stream);
         CK(cudaStreamSynchronize(s));
         CK(cudaStreamSynchronize(h->copy_stream));
-        if (bad) throw InvalidArg("non-finite entry in v");
+        if (trace) {
+            const double host_ms = std::chrono::duration<double, std::milli>(
+                                       std::chrono::steady_clock::now() - t_host0).count();
+            fprintf(stderr, "entries trace: host %.3f ms | device:", host_ms);
+            for (int k = 1; k < nev; ++k) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, ev[0], ev[k]);
+                fprintf(stderr, " %.3f", ms);
+            }
+            fprintf(stderr, " (H2D v, staged v, pieces..., D2H)\n");
+            for (int k = 0; k < nev; ++k) cudaEventDestroy(ev[k]);
+        }
+        if ((unsigned int)res[0]) throw InvalidArg("non-finite entry in v");
+        if (total_jumps) *total_jumps = res[1];
         return;
     }
     const uint32_t* rd;
@@ -549,6 +595,11 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
     CK(cudaMemcpyAsync(se, os, nrows * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(jumps, oj, nrows * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (total_jumps) {
+        uint64_t t = 0;
+        for (uint64_t r = 0; r < nrows; ++r) t += jumps[r];
+        *total_jumps = t;
+    }
 }
 
 // Theorem 2 walkers (vector / tc).  start_mode 0 uniform, 1 categorical.
@@ -933,10 +984,11 @@ int expmc_cuda_entry_estimate(expmc_matrix* h, const double* v, uint64_t nv, uin
 
 int expmc_cuda_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* rows,
                        uint64_t nrows, const expmc_path_params* p, double* value,
-                       double* std_error, uint64_t* jumps) {
+                       double* std_error, uint64_t* jumps, uint64_t* total_jumps) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
-        run_entries(h, v, nv, rows, nrows, p, value, std_error, jumps);
+        if (total_jumps) *total_jumps = 0;
+        run_entries(h, v, nv, rows, nrows, p, value, std_error, jumps, total_jumps);
     });
 }
 

@@ -122,6 +122,7 @@ void launch_final_reduce(const double* part_a, const double* part_b,
                          double* out_b, unsigned long long* out_c, cudaStream_t s);
 void launch_scale(uint64_t n, double* x, double alpha, cudaStream_t s);
 void launch_count_nonfinite(uint64_t n, const double* x, unsigned int* flag, cudaStream_t s);
+void launch_sum_u64(uint64_t n, const uint64_t* x, unsigned long long* out, cudaStream_t s);
 
 // expmv.cu (K5)
 void launch_spmv(const DevSplit& m, int mode, double shift, const double* x, double* y,

@@ -54,6 +54,25 @@ __global__ void nonfinite_kernel(uint64_t n, const double* __restrict__ x,
 
 }  // namespace
 
+// *out += sum of x[0..n) (integer: exact and order-independent)
+__global__ void sum_u64_kernel(const uint64_t* __restrict__ x, uint64_t n,
+                               unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        acc += x[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+void launch_sum_u64(uint64_t n, const uint64_t* x, unsigned long long* out, cudaStream_t s) {
+    if (!n) return;
+    const uint64_t want = (n + 255) / 256;
+    const unsigned grid = (unsigned)(want < 148 * 8 ? want : 148 * 8);
+    sum_u64_kernel<<<grid, 256, 0, s>>>(x, n, out);
+}
+
 void launch_count_nonfinite(uint64_t n, const double* x, unsigned int* flag, cudaStream_t s) {
     if (n == 0) return;
     nonfinite_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, x, flag);

@@ -105,16 +105,14 @@ class VectorEstimate:
 @dataclass
 class EntriesEstimate:
     """Batched entry_estimate over many rows ("full vector with W walkers
-    per entry"): per-row value, standard error and jump count."""
-    rows: np.ndarray
+    per entry"): per-row value, standard error and jump count.  ``rows`` is
+    None for the full vector (row k = entry k)."""
+    rows: np.ndarray | None
     values: np.ndarray
     std_errors: np.ndarray
     jumps: np.ndarray
     samples_per_entry: int
-
-    @property
-    def total_jumps(self) -> int:
-        return int(self.jumps.sum())
+    total_jumps: int  # sum of jumps (reduced on the device)
 
 
 def _f64(a):
@@ -259,7 +257,7 @@ def entries_estimate(m: SplitMatrix, v, rows, p: PathParams, out=None) -> Entrie
     if rows is None:
         nrows = m.n
         rp = None
-        rows_arr = np.arange(m.n, dtype=np.uint32)
+        rows_arr = None
     else:
         rows_arr = np.asarray(rows)
         if rows_arr.size and (rows_arr.min() < 0 or rows_arr.max() >= 2**32):
@@ -276,10 +274,12 @@ def entries_estimate(m: SplitMatrix, v, rows, p: PathParams, out=None) -> Entrie
                 and jm.dtype in (np.uint64, np.int64) and val.flags.c_contiguous
                 and se.flags.c_contiguous and jm.flags.c_contiguous):
             raise ValueError("out arrays must be contiguous f64/f64/u64 of length >= nrows")
+    tot = C.c_uint64()
     check(lib().expmc_cuda_entries(m.handle, v.ctypes.data_as(f64p), len(v), rp, nrows,
                                    C.byref(pc), val.ctypes.data_as(f64p),
-                                   se.ctypes.data_as(f64p), jm.ctypes.data_as(u64p)))
-    return EntriesEstimate(rows_arr, val, se, jm, p.samples)
+                                   se.ctypes.data_as(f64p), jm.ctypes.data_as(u64p),
+                                   C.byref(tot)))
+    return EntriesEstimate(rows_arr, val, se, jm, p.samples, tot.value)
 
 
 def vector_estimate(m: SplitMatrix, v, p: PathParams, workers: int = 1) -> VectorEstimate:
