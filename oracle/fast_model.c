@@ -187,9 +187,10 @@ static double fm_walker(const fm_rec* rec, const uint32_t* nbr, const uint32_t* 
     }
 }
 
-/* Accumulation contract of the kernel: lane s of warp w (of WPR = T/32
- * warps) sums walkers l = s (mod 32) with floor(l/128) = w (mod WPR) in
- * increasing l; xor butterfly over lanes; warps in index order. */
+/* Accumulation contract of the kernel: part w (of WPR = T/32 parts) owns
+ * the walkers l with floor(l/128) = w (mod WPR).  Its jumpers, numbered
+ * k = 0, 1, ... in increasing l, are summed by lane k mod 32 in increasing k;
+ * xor butterfly over lanes; parts in index order. */
 void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
                 const uint32_t* thr, const uint32_t* alias, const uint32_t* rows,
                 uint64_t nrows, double beta, uint64_t N, uint64_t W, int strang,
@@ -217,6 +218,7 @@ void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
             uint64_t bj[32];
             for (int s = 0; s < 32; ++s) { b1[s] = 0.0; b2[s] = 0.0; bj[s] = 0; }
             uint32_t n0 = 0; /* never-jumpers of this part */
+            uint64_t nj = 0; /* jumpers of this part so far */
             for (uint64_t c = wi; c < nch; c += wpr) {
                 for (int q = 0; q < 4; ++q) {
                     for (int s = 0; s < 32; ++s) {
@@ -231,9 +233,10 @@ void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
                             ++n0;
                             continue; /* exact zero: skipped (bit-identical) */
                         }
-                        b1[s] = b1[s] + dev;
-                        b2[s] = fma(dev, dev, b2[s]);
-                        bj[s] += jl;
+                        const int ln = (int)(nj++ % 32);
+                        b1[ln] = b1[ln] + dev;
+                        b2[ln] = fma(dev, dev, b2[ln]);
+                        bj[ln] += jl;
                     }
                 }
             }

@@ -20,18 +20,19 @@
 //  * Warp-cooperative scheduling over a stream of tasks.  Task t = (row
 //    t / WPR, part t % WPR) owns the row's chunks c ≡ part (mod WPR) of 128
 //    walkers.  A warp sweeps chunks (one Philox block per lane) and appends
-//    the jumpers as tickets to a shared-memory ring of kCap tickets (up to
-//    kRing chunks in flight); idle lanes pop tickets in order, across chunk
-//    and row boundaries, so the sojourn code runs with (nearly) full warps.
-//    A finishing walker only parks its raw weight sum S, end value v and
-//    jump count in its ticket; chunks are finalized strictly in order: the
-//    exponent, exp() and deviation are computed convergently over the
-//    chunk's tickets, scattered to a 128-slot buffer, and lane s adds slots
-//    s, s+32, s+64, s+96 (non-jumper zeros skipped: adding +0.0 never
-//    changes such a sum).
+//    the jumpers as tickets to a shared-memory ring of CAP tickets (up to
+//    ENTRY_TASKS tasks in flight); idle lanes pop tickets in order, across
+//    chunk and row boundaries, so the sojourn code runs with (nearly) full
+//    warps.  A finishing walker only parks its raw weight sum S, end value v
+//    and jump count in its ticket.  Tickets of a task are contiguous, so they
+//    are accumulated in batches of 32 consecutive tickets of the oldest task
+//    (exponent, exp() and deviation convergent over the batch, ticket k of
+//    the task on lane k mod 32, straight into that lane's running sums), and
+//    a task is finalized once its last batch is in.
 //  * Fixed accumulation order (result contract, replayed by
-//    oracle/fast_model.c): lane s of part w of a row sums the walkers
-//    l ≡ s (mod 32) with floor(l/128) ≡ w (mod WPR) in increasing l; lanes are
+//    oracle/fast_model.c): part w of a row owns the walkers with
+//    floor(l/128) ≡ w (mod WPR); its jumpers, numbered k = 0, 1, ... in
+//    increasing l, are summed by lane k mod 32 in increasing k; lanes are
 //    combined by an xor butterfly, parts in index order.  Independent of
 //    scheduling, grid shape, GPU count and row sharding.
 #include <cmath>
@@ -48,10 +49,10 @@ constexpr int kChunk = 128;
 constexpr unsigned FULL = 0xffffffffu;
 
 #ifndef ENTRY_MIN_BLOCKS
-#define ENTRY_MIN_BLOCKS 6
+#define ENTRY_MIN_BLOCKS 7
 #endif
-#ifndef ENTRY_RING
-#define ENTRY_RING 8    // chunks in flight per warp (power of 2)
+#ifndef ENTRY_TASKS
+#define ENTRY_TASKS 8   // tasks in flight per warp (power of 2, <= 8: slot in 3 ticket bits)
 #endif
 #ifndef ENTRY_CAP
 #define ENTRY_CAP 256   // jumper tickets in flight per warp (power of 2, >= 128)
@@ -73,38 +74,33 @@ struct RowRecU {     // RowRec without its 32-byte alignment (smem copy)
     double d, v;
 };
 
-struct RowConst {    // per task: the start row and its constants (9 words)
-    RowRecU rr;      // record of the row                          words 0-3
-    uint32_t i;      // matrix row                                 word 4
-    uint32_t chunk;  // chunk index (ChunkMeta only)
-    uint32_t T0;     // never-jump threshold on a u32 draw          word 5
-    uint32_t dead;   // 1: e^{-rate β} rounds to 1, no walker ever jumps
+// One task in flight (row, part): the start row's constants and the task's
+// ticket range.  Tickets of a task are contiguous in ticket-counter space
+// (chunks are admitted task by task), so the accumulation lane of a jumper
+// is its part-local jumper index mod 32 = (ticket - tstart) mod 32.
+struct TaskRec {
+    RowRecU rr;      // record of the start row
+    uint32_t i;      // matrix row
+    uint32_t nw;     // walkers of the task part
+    uint32_t tstart; // first ticket of the task
+    uint32_t tend;   // one past its last ticket (valid once closed)
+    uint32_t task;   // task id (row index in the launch, times WPR, plus part)
+    uint32_t closed; // all chunks swept
     double f0;       // e^{β d_i} v_i (score of a walker that never jumps)
     double K;        // shift of the deviation sums: f0 when never-jumpers are the
                      // majority (T0 >= 2^31), else 0 (no cancellation against a
                      // huge f0 that no walker realises, e.g. BA hubs)
     double corr;     // weight correction at the start state (½ d_i Strang, d_i Lie)
 };
-constexpr int kRowWords = 9;
+static_assert(sizeof(TaskRec) == 80, "task layout");
 
-struct ChunkMeta {
-    RowConst row;           // row.chunk = chunk index within the row   words 0-8
-    uint32_t tstart, tend;  // the chunk's ticket range (counters)       word 9
-    uint32_t task;          // task id                                   word 10
-    uint32_t last;          // last chunk of its task
-    uint32_t jm[4];         // jumper bitmask of slots 32q + lane          words 11-12
-};
-static_assert(sizeof(RowConst) == 8 * kRowWords && sizeof(ChunkMeta) == 104, "meta layout");
-
-template <int R, int CAP>
+template <int RT, int CAP>
 struct WarpState {
     double S[CAP];      // per ticket: raw weight sum at finish
     double v[CAP];      // per ticket: v at the end state
-    uint2 tk[CAP];      // per ticket: {decision word until started, then jump
-                        //   count; ring slot << 8 | chunk slot}
-    double dev[kChunk]; // finalize scatter buffer (slot order)
-    ChunkMeta meta[R];
-    RowConst adm;       // row of the task being admitted
+    uint2 tk[CAP];      // per ticket: {decision word (low 3 bits: task slot) until
+                        //   popped, then the jump count; walker index l}
+    TaskRec task[RT];
 };
 
 #ifdef ENTRY_STATS
@@ -120,53 +116,35 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                   uint64_t nrows, FastParams p, double* __restrict__ out_value,
                   double* __restrict__ out_se, uint64_t* __restrict__ out_jumps,
                   double4* __restrict__ partial) {
-    constexpr int R = ENTRY_RING;
+    constexpr int RT = ENTRY_TASKS;
     constexpr uint32_t CAP = ENTRY_CAP;
-    static_assert((R & (R - 1)) == 0 && (CAP & (CAP - 1)) == 0 && CAP >= kChunk, "ring sizes");
+    static_assert((RT & (RT - 1)) == 0 && RT <= 8 && (CAP & (CAP - 1)) == 0 && CAP >= kChunk,
+                  "ring sizes");
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
-    __shared__ WarpState<R, CAP> states[4];
-    WarpState<R, CAP>& q = states[warp];
+    __shared__ WarpState<RT, CAP> states[4];
+    WarpState<RT, CAP>& q = states[warp];
     const uint32_t nch = (uint32_t)((p.W + kChunk - 1) / kChunk);
     const uint32_t ntask = (uint32_t)(nrows * WPR);
     const uint32_t tstride = gridDim.x * 4u;
 
-    // admission cursor (warp-uniform); the task's row constants live in smem
-    uint32_t atask = blockIdx.x * 4u + warp;
+    // task ring (warp-uniform counters): tasks [tf, tw) are in flight, the
+    // newest is being swept while `aopen`
+    uint32_t tw = 0, tf = 0;
+    bool aopen = false;
+    uint32_t atask = blockIdx.x * 4u + warp;  // next task to open / the open task
     uint32_t achunk = 0;
-    auto load_task = [&](uint32_t t) {
-        achunk = t % WPR;
-        if (lane == 0) {
-            RowConst& a = q.adm;
-            const uint32_t i = rows[t / WPR];
-            const RowRec ri = load_rec(rec, i);
-            const double p0 = exp_det(-__dmul_rn(__ldg(rate + i), p.beta));
-            const unsigned long long T0 = (unsigned long long)__dmul_rn(p0, 4294967296.0);
-            a.rr = RowRecU{ri.off, ri.deg_flags, ri.inv_rate, 0u, ri.d, ri.v};
-            a.i = i;
-            a.T0 = (uint32_t)T0;
-            a.dead = T0 >> 32 ? 1u : 0u;  // T0 = 2^32: never jumps
-            a.f0 = __dmul_rn(exp_det(__dmul_rn(p.beta, ri.d)), ri.v);
-            a.K = T0 >= (1ull << 31) ? a.f0 : 0.0;
-            a.corr = p.strang ? __dmul_rn(0.5, ri.d) : ri.d;
-        }
-        __syncwarp();
-    };
-    if (atask < ntask) load_task(atask);
-
-    int oldest = 0, live = 0;
     uint32_t head = 0, tail = 0;  // ticket counters (positions mod CAP)
-    uint32_t tbase = 0;           // first ticket of the oldest live chunk (= tail if none)
+    uint32_t xc = 0;              // accumulation cursor: tickets before it are summed
     // lane-private walker state
     bool act = false;
-    uint32_t tk = 0, rsl = 0, off = 0, degf = 0, G = 0, jc = 0, ew = 0;
+    uint32_t tk = 0, wl = 0, wi = 0, off = 0, degf = 0, G = 0, jc = 0, ew = 0;
     float ir = 0.f;
     double dcur = 0.0, vcur = 0.0, t = 0.0, S = 0.0;
-    // per-task accumulators (tasks finalize in order)
+    // per-task accumulators of the oldest task (lane = jumper index mod 32)
     double s1 = 0.0, s2 = 0.0;
     unsigned long long jsum = 0;
-    uint32_t nwt = 0, njt = 0;  // walkers / jumpers of the task part (warp-uniform)
 
     // One sojourn of the lane's walker from its current state: either the
     // path ends (park S', v, jumps in the ticket; lane becomes idle) or the
@@ -175,7 +153,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         const float h = __fmul_rn(neg_ln_u(ew), ir);
         const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
         if (tn >= p.n_grid) {
-            // park the raw weight sum; the exponent is formed at finalize
+            // park the raw weight sum; the exponent is formed at accumulation
             S = __fma_rn(dcur, (double)(p.N + 1 - G), S);
             const uint32_t pos = tk & (CAP - 1);
             q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, dcur)) : S;
@@ -192,54 +170,87 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         }
     };
 
-    // Sweep the next chunk of the admission task: decide its walkers and
-    // append the jumpers as tickets (ring slot rs = next meta slot).
-    auto can_admit = [&] {
-        return live < R && atask < ntask && tail + kChunk - tbase <= CAP;
+    // Open task `atask` in slot tw: row constants computed by two lanes in
+    // parallel (lane 0: e^{-rate β}, lane 1: e^{β d}).
+    auto open_task = [&] {
+        const int sl = (int)(tw & (RT - 1));
+        const uint32_t i = rows[atask / WPR];
+        const RowRec ri = load_rec(rec, i);
+        const double rt = __ldg(rate + i);
+        const double ex = exp_det(lane == 0 ? -__dmul_rn(rt, p.beta) : __dmul_rn(p.beta, ri.d));
+        const double e0 = __shfl_sync(FULL, ex, 0), e1 = __shfl_sync(FULL, ex, 1);
+        const unsigned long long T0 = (unsigned long long)__dmul_rn(e0, 4294967296.0);
+        const uint32_t part = atask % WPR;
+        const uint32_t ncp = nch > part ? (nch - part + WPR - 1) / WPR : 0u;  // chunks of the part
+        const uint64_t lastb = (uint64_t)(part + (ncp - 1) * WPR) * kChunk;   // its last chunk
+        const uint32_t nw = ncp == 0 ? 0u
+                                      : (ncp - 1) * kChunk +
+                                            (uint32_t)(p.W - lastb < (uint64_t)kChunk ? p.W - lastb
+                                                                                     : kChunk);
+        const bool dead = (T0 >> 32) != 0 || ncp == 0;  // T0 = 2^32: never jumps
+        if (lane == 0) {
+            TaskRec& a = q.task[sl];
+            a.rr = RowRecU{ri.off, ri.deg_flags, ri.inv_rate, (uint32_t)T0, ri.d, ri.v};
+            a.i = i;
+            a.nw = nw;
+            a.tstart = tail;
+            a.tend = tail;
+            a.task = atask;
+            a.closed = dead ? 1u : 0u;
+            const double f0 = __dmul_rn(e1, ri.v);
+            a.f0 = f0;
+            a.K = T0 >= (1ull << 31) ? f0 : 0.0;
+            a.corr = p.strang ? __dmul_rn(0.5, ri.d) : ri.d;
+        }
+        ++tw;
+        achunk = part;
+        if (dead) {
+            atask += tstride;
+        } else {
+            aopen = true;
+        }
+        __syncwarp();
     };
-    auto admit_chunk = [&] {
-        const int rs = (oldest + live) & (R - 1);
+
+    // Sweep the next chunk of the open task: decide its walkers and append the
+    // jumpers as tickets.
+    auto can_admit = [&] {
+        return aopen ? tail + kChunk - xc <= CAP : (atask < ntask && tw - tf < (uint32_t)RT);
+    };
+    auto admit = [&] {
+        if (!aopen) {
+            open_task();
+            return;
+        }
+        const uint32_t sl = (tw - 1) & (RT - 1);
+        const TaskRec& a = q.task[sl];
         const uint32_t base = achunk * kChunk;
         const uint64_t rem = p.W - base;
         const uint32_t nw = rem < (uint64_t)kChunk ? (uint32_t)rem : (uint32_t)kChunk;
-        const uint32_t lim = q.adm.dead ? 0u : nw;  // walkers that may jump
-        const uint32_t T0 = q.adm.T0;
-        const U4 D = philox4x32_10(
-            U4{0xffffffffu, base + (uint32_t)lane, q.adm.i, kTagEntry}, p.rk);
+        const uint32_t T0 = a.rr.spare;
+        const U4 D = philox4x32_10(U4{0xffffffffu, base + (uint32_t)lane, a.i, kTagEntry}, p.rk);
         const uint32_t wd[4] = {D.x, D.y, D.z, D.w};
-        const uint32_t t0 = tail;
-        unsigned bq[4];
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) {
-            const uint32_t sl = 32u * qq + lane;
-            const bool jmp = sl < lim && wd[qq] >= T0;
+            const uint32_t l = 32u * qq + lane;
+            const bool jmp = l < nw && wd[qq] >= T0;
             const unsigned b = __ballot_sync(FULL, jmp);
-            bq[qq] = b;
             if (jmp) q.tk[(tail + __popc(b & lt)) & (CAP - 1)] =
-                         make_uint2(wd[qq], ((uint32_t)rs << 8) | sl);
+                         make_uint2((wd[qq] & ~7u) | sl, base + l);
             tail += __popc(b);
         }
         const uint32_t nextc = achunk + WPR;
-        {   // chunk meta: one 8-byte word per lane
-            uint64_t* dst = reinterpret_cast<uint64_t*>(&q.meta[rs]);
-            const uint64_t* src = reinterpret_cast<const uint64_t*>(&q.adm);
-            uint64_t x = 0;
-            if (lane < kRowWords) x = src[lane];
-            if (lane == 4) x = (x & 0xffffffffull) | ((uint64_t)achunk << 32);
-            if (lane == 9) x = t0 | ((uint64_t)tail << 32);
-            if (lane == 10) x = atask | ((uint64_t)(nextc >= nch) << 32);
-            if (lane == 11) x = bq[0] | ((uint64_t)bq[1] << 32);
-            if (lane == 12) x = bq[2] | ((uint64_t)bq[3] << 32);
-            if (lane < 13) dst[lane] = x;
-        }
-        __syncwarp();
-        ++live;
         if (nextc < nch) {
             achunk = nextc;
-        } else {
+        } else {  // task fully swept
+            if (lane == 0) {
+                q.task[sl].tend = tail;
+                q.task[sl].closed = 1u;
+            }
+            aopen = false;
             atask += tstride;
-            if (atask < ntask) load_task(atask);
         }
+        __syncwarp();
     };
 
     while (true) {
@@ -253,7 +264,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         if (idle) {
             // ---- admit: sweep chunks while queued tickets cannot feed the
             // idle lanes and a whole chunk's tickets fit in the ring
-            while (can_admit() && tail - head < (uint32_t)__popc(idle)) admit_chunk();
+            while (can_admit() && tail - head < (uint32_t)__popc(idle)) admit();
             // ---- pop: idle lanes take tickets in order
             const uint32_t avail = tail - head;
             const uint32_t nidle = (uint32_t)__popc(idle);
@@ -262,11 +273,12 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             if (!act && rank < take) {
                 tk = head + rank;
                 const uint2 t2 = q.tk[tk & (CAP - 1)];
-                rsl = t2.y;
                 ew = t2.x;
-                const ChunkMeta& m = q.meta[rsl >> 8];
-                off = m.row.rr.off; degf = m.row.rr.deg_flags;
-                ir = m.row.rr.inv_rate; dcur = m.row.rr.d; vcur = m.row.rr.v;
+                wl = t2.y;
+                const TaskRec& m = q.task[t2.x & 7u];
+                off = m.rr.off; degf = m.rr.deg_flags;
+                ir = m.rr.inv_rate; dcur = m.rr.d; vcur = m.rr.v;
+                wi = m.i;
                 t = 0.0; S = 0.0; G = 0; jc = 0;
                 act = true;
                 // a jumper's first sojourn ends in a jump (decision word >= T0),
@@ -297,102 +309,85 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
 #endif
         // ---- C: one jump for every walker whose sojourn did not end the path
         if (jmp) {
-            const ChunkMeta& m = q.meta[rsl >> 8];
-            const U4 B = philox4x32_10(
-                U4{jc, m.row.chunk * kChunk + (rsl & 255u), m.row.i, kTagEntry}, p.rk);
+            const U4 B = philox4x32_10(U4{jc, wl, wi, kTagEntry}, p.rk);
             const Edge e = jump_edge(B.y, B.w, B.z, off, degf, adj, thr, alias);
             ew = B.x;
             ++jc;
             off = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d; vcur = e.v;
         }
-#if ENTRY_PREFETCH
-        // ---- refill the ring while this iteration's gathers are in flight
-        // (the pops before the next jump then rarely have to sweep)
-        while (can_admit() && tail - head < (uint32_t)ENTRY_PREFETCH) admit_chunk();
-#endif
-        // ---- finalize the oldest chunks once all their walkers are done
-        // (the condition can only change in an iteration that popped a
-        // ticket or retired a walker)
+        // ---- accumulate finished tickets in batches of 32 (lane = ticket -
+        // tstart mod 32) and finalize completed tasks, oldest first.  The
+        // condition can only change in an iteration that popped a ticket or
+        // retired a walker.
         if (!(idle | __ballot_sync(FULL, fin))) continue;
         __syncwarp();
-        // oldest ticket still walking, as an offset from tbase (~0: none);
-        // a chunk is done once all its tickets are popped and none walks
-        const uint32_t base0 = tbase;
+        // oldest ticket still walking, as an offset from xc (~0: none)
+        const uint32_t base0 = xc;
         const uint32_t minoff = __reduce_min_sync(FULL, act ? tk - base0 : ~0u);
-        while (live > 0) {
-            const ChunkMeta& m = q.meta[oldest];
-            const uint32_t ts = m.tstart, te = m.tend;
-            if ((int)(head - te) < 0 || te - base0 > minoff) break;
-            const double f0 = m.row.f0, K = m.row.K, corr = m.row.corr;
-            const uint64_t base = (uint64_t)m.row.chunk * kChunk;
-            unsigned long long jl = 0;
-            for (uint32_t k = ts + lane; k < te; k += 32) {
-                const uint32_t pos = k & (CAP - 1);
-                const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], corr));
-                const uint2 t2 = q.tk[pos];
-                q.dev[t2.y & 255u] = __dsub_rn(__dmul_rn(exp_det(x), q.v[pos]), K);
-                jl += t2.x;
-            }
-            __syncwarp();
-#pragma unroll
-            for (int qq = 0; qq < 4; ++qq) {
-                const uint32_t sl = 32u * qq + lane;
-                // non-jumper slots contribute exact zeros: skipped (bit-identical)
-                if ((m.jm[qq] >> lane) & 1u) {
-                    const double dv = q.dev[sl];
+        while (tf != tw) {
+            const TaskRec& m = q.task[tf & (RT - 1)];
+            const bool closed = m.closed != 0u;
+            const uint32_t lim = closed ? m.tend : tail;
+            if (xc != lim) {
+                const uint32_t be = lim - xc < 32u ? lim : xc + 32u;  // batch end
+                // an open task waits for a full batch; every ticket of the batch
+                // must be popped and none may still walk
+                if ((!closed && be - xc < 32u) || (int)(head - be) < 0 || be - base0 > minoff)
+                    break;
+                const uint32_t k = xc + lane;
+                if (k < be) {
+                    const uint32_t pos = k & (CAP - 1);
+                    const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], m.corr));
+                    const double dv = __dsub_rn(__dmul_rn(exp_det(x), q.v[pos]), m.K);
                     s1 = __dadd_rn(s1, dv);
                     s2 = __fma_rn(dv, dv, s2);
+                    jsum += q.tk[pos].x;
                 }
+                xc = be;
+                continue;
             }
-            jsum += jl;
-            njt += te - ts;
-            nwt += (uint32_t)(p.W - base < (uint64_t)kChunk ? p.W - base : (uint64_t)kChunk);
-            tbase = te;  // the next chunk's tickets start where this one's end
-            if (m.last) {
+            if (!closed) break;  // the open task has no pending tickets
+            // task complete: butterfly, never-jumpers, output
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    s1 = __dadd_rn(s1, __shfl_xor_sync(FULL, s1, o));
-                    s2 = __dadd_rn(s2, __shfl_xor_sync(FULL, s2, o));
-                    jsum += __shfl_xor_sync(FULL, jsum, o);
-                }
-                if (lane == 0) {
-                    // never-jumpers score f0: deviation f0 - K each (0 when K = f0)
-                    const uint32_t n0 = nwt - njt;
-                    const double c = __dsub_rn(f0, K);
-                    if (n0 != 0 && c != 0.0) {
-                        s1 = __fma_rn((double)n0, c, s1);
-                        s2 = __fma_rn((double)n0, __dmul_rn(c, c), s2);
-                    }
-                    const uint64_t task = m.task;
-                    if (WPR == 1) {
-                        const double W = (double)p.W;
-                        out_value[task] = __dadd_rn(K, __ddiv_rn(s1, W));
-                        double se = 0.0;
-                        if (p.W > 1) {
-                            double var =
-                                __ddiv_rn(__dsub_rn(s2, __ddiv_rn(__dmul_rn(s1, s1), W)),
-                                          __dsub_rn(W, 1.0));
-                            var = var > 0.0 ? var : 0.0;
-                            se = sqrt(__ddiv_rn(var, W));
-                        }
-                        out_se[task] = se;
-                        out_jumps[task] = jsum;
-                    } else {
-                        partial[task] = make_double4(s1, s2, __longlong_as_double((long long)jsum),
-                                                     K);
-                    }
-                }
-                s1 = 0.0;
-                s2 = 0.0;
-                jsum = 0;
-                nwt = 0;
-                njt = 0;
+            for (int o = 16; o > 0; o >>= 1) {
+                s1 = __dadd_rn(s1, __shfl_xor_sync(FULL, s1, o));
+                s2 = __dadd_rn(s2, __shfl_xor_sync(FULL, s2, o));
+                jsum += __shfl_xor_sync(FULL, jsum, o);
             }
+            if (lane == 0) {
+                // never-jumpers score f0: deviation f0 - K each (0 when K = f0)
+                const double f0 = m.f0, K = m.K;
+                const uint32_t n0 = m.nw - (m.tend - m.tstart);
+                const double c = __dsub_rn(f0, K);
+                if (n0 != 0 && c != 0.0) {
+                    s1 = __fma_rn((double)n0, c, s1);
+                    s2 = __fma_rn((double)n0, __dmul_rn(c, c), s2);
+                }
+                const uint64_t task = m.task;
+                if (WPR == 1) {
+                    const double W = (double)p.W;
+                    out_value[task] = __dadd_rn(K, __ddiv_rn(s1, W));
+                    double se = 0.0;
+                    if (p.W > 1) {
+                        double var = __ddiv_rn(__dsub_rn(s2, __ddiv_rn(__dmul_rn(s1, s1), W)),
+                                               __dsub_rn(W, 1.0));
+                        var = var > 0.0 ? var : 0.0;
+                        se = sqrt(__ddiv_rn(var, W));
+                    }
+                    out_se[task] = se;
+                    out_jumps[task] = jsum;
+                } else {
+                    partial[task] =
+                        make_double4(s1, s2, __longlong_as_double((long long)jsum), K);
+                }
+            }
+            s1 = 0.0;
+            s2 = 0.0;
+            jsum = 0;
+            ++tf;
             __syncwarp();
-            oldest = (oldest + 1) & (R - 1);
-            --live;
         }
-        if (live == 0 && atask >= ntask) break;  // every chunk of every task finalized
+        if (tf == tw && !aopen && atask >= ntask) break;  // every task finalized
     }
 }
 
@@ -432,11 +427,12 @@ int launch_t(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const Fast
              double* value, double* se, uint64_t* jumps, double4* partial, cudaStream_t s) {
     // Exactly ENTRY_MIN_BLOCKS resident blocks per SM with the smallest
     // shared-memory carveout that holds them, so the rest of the SM's 256 KB
-    // is L1 for the edge gathers.  The driver sizes the carveout for the
-    // maximum occupancy, which the register count alone would put at 7
-    // blocks (228 KB carveout, ~28 KB L1: measured 1.8x slower on the
-    // L1-local config 4); padding each block with dynamic shared memory so
-    // that a 7th block cannot fit pins 6 blocks at a 196 KB carveout.
+    // is L1 for the edge gathers, and no more: padding each block with
+    // dynamic shared memory so that an extra block cannot fit pins the block
+    // count (when the driver sized the carveout for a register-limited
+    // occupancy above the target, config 4 ran 1.8x slower).  v10 (72 regs,
+    // 27 KB smem per block) measured best at 7 blocks: config 5 81.9 -> 77.3
+    // ms, config 4 4.97 -> 4.67 s against 6 blocks.
     // Grid = one wave of resident blocks (the kernel strides over tasks).
     static int nsm = 0, pad = 0;
     if (!nsm) {
