@@ -82,10 +82,10 @@ struct TaskRec {
     RowRecU rr;      // record of the start row
     uint32_t i;      // matrix row
     uint32_t nw;     // walkers of the task part
-    uint32_t tstart; // first ticket of the task
     uint32_t tend;   // one past its last ticket (valid once closed)
+    uint32_t closed; // all chunks swept (read with tend as one 8-byte word)
+    uint32_t tstart; // first ticket of the task
     uint32_t task;   // task id (row index in the launch, times WPR, plus part)
-    uint32_t closed; // all chunks swept
     double f0;       // e^{β d_i} v_i (score of a walker that never jumps)
     double K;        // shift of the deviation sums: f0 when never-jumpers are the
                      // majority (T0 >= 2^31), else 0 (no cancellation against a
@@ -98,8 +98,12 @@ template <int RT, int CAP>
 struct WarpState {
     double S[CAP];      // per ticket: raw weight sum at finish
     double v[CAP];      // per ticket: v at the end state
-    uint2 tk[CAP];      // per ticket: {decision word (low 3 bits: task slot) until
-                        //   popped, then the jump count; walker index l}
+    uint2 tk[CAP + 1];  // per ticket: {decision word (low 3 bits: task slot) until
+                        //   popped, then the jump count; walker index l}; the
+                        //   last is the sink of the sweep's unconditional stores
+                        //   (7 blocks x (smem + 1 KB) must stay under the 196 KB
+                        //   carveout: 1 KB more moved config 4 to a 28 KB L1 and
+                        //   1.86x the time)
     TaskRec task[RT];
 };
 
@@ -235,8 +239,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             const uint32_t l = 32u * qq + lane;
             const bool jmp = l < nw && wd[qq] >= T0;
             const unsigned b = __ballot_sync(FULL, jmp);
-            if (jmp) q.tk[(tail + __popc(b & lt)) & (CAP - 1)] =
-                         make_uint2((wd[qq] & ~7u) | sl, base + l);
+            // branch-free: non-jumpers store to the sink slot
+            const uint32_t pos = jmp ? ((tail + __popc(b & lt)) & (CAP - 1)) : CAP;
+            q.tk[pos] = make_uint2((wd[qq] & ~7u) | sl, base + l);
             tail += __popc(b);
         }
         const uint32_t nextc = achunk + WPR;
@@ -321,19 +326,24 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         // retired a walker.
         if (!(idle | __ballot_sync(FULL, fin))) continue;
         __syncwarp();
-        // oldest ticket still walking, as an offset from xc (~0: none)
-        const uint32_t base0 = xc;
-        const uint32_t minoff = __reduce_min_sync(FULL, act ? tk - base0 : ~0u);
+        // tickets before `ready` are popped and finished: the oldest ticket
+        // still walking (or the first not popped) bounds it
+        const uint32_t minoff = __reduce_min_sync(FULL, act ? tk - xc : ~0u);
+        const uint32_t ready = head - xc < minoff ? head : xc + minoff;
         while (tf != tw) {
             const TaskRec& m = q.task[tf & (RT - 1)];
-            const bool closed = m.closed != 0u;
-            const uint32_t lim = closed ? m.tend : tail;
-            if (xc != lim) {
-                const uint32_t be = lim - xc < 32u ? lim : xc + 32u;  // batch end
-                // an open task waits for a full batch; every ticket of the batch
-                // must be popped and none may still walk
-                if ((!closed && be - xc < 32u) || (int)(head - be) < 0 || be - base0 > minoff)
-                    break;
+            const uint2 ec = *reinterpret_cast<const uint2*>(&m.tend);  // {tend, closed}
+            // tickets of this task that are ready
+            const uint32_t lim = ec.y && ec.x - xc < ready - xc ? ec.x : ready;
+            uint32_t be;
+            if (lim - xc >= 32u) {
+                be = xc + 32u;                // a full batch
+            } else if (ec.y && lim == ec.x) {
+                be = lim;                     // the closed task's last (partial) batch
+            } else {
+                break;                        // wait for more tickets
+            }
+            if (be != xc) {
                 const uint32_t k = xc + lane;
                 if (k < be) {
                     const uint32_t pos = k & (CAP - 1);
@@ -344,9 +354,8 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                     jsum += q.tk[pos].x;
                 }
                 xc = be;
-                continue;
             }
-            if (!closed) break;  // the open task has no pending tickets
+            if (!ec.y || xc != ec.x) continue;
             // task complete: butterfly, never-jumpers, output
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
