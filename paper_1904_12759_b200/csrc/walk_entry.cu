@@ -78,7 +78,7 @@ struct RowRecU {     // RowRec without its 32-byte alignment (smem copy)
 // ticket range.  Tickets of a task are contiguous in ticket-counter space
 // (chunks are admitted task by task), so the accumulation lane of a jumper
 // is its part-local jumper index mod 32 = (ticket - tstart) mod 32.
-struct TaskRec {
+struct __align__(16) TaskRec {
     RowRecU rr;      // record of the start row
     uint32_t i;      // matrix row
     uint32_t nw;     // walkers of the task part
@@ -98,13 +98,13 @@ template <int RT, int CAP>
 struct WarpState {
     double S[CAP];      // per ticket: raw weight sum at finish
     double v[CAP];      // per ticket: v at the end state
+    TaskRec task[RT];   // (16-byte aligned: the pop reads rr as one uint4)
     uint2 tk[CAP + 1];  // per ticket: {decision word (low 3 bits: task slot) until
                         //   popped, then the jump count; walker index l}; the
                         //   last is the sink of the sweep's unconditional stores
                         //   (7 blocks x (smem + 1 KB) must stay under the 196 KB
                         //   carveout: 1 KB more moved config 4 to a 28 KB L1 and
                         //   1.86x the time)
-    TaskRec task[RT];
 };
 
 #ifdef ENTRY_STATS
@@ -143,9 +143,16 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     uint32_t xc = 0;              // accumulation cursor: tickets before it are summed
     // lane-private walker state
     bool act = false;
-    uint32_t tk = 0, wl = 0, wi = 0, off = 0, degf = 0, G = 0, jc = 0, ew = 0;
-    float ir = 0.f;
-    double dcur = 0.0, vcur = 0.0, t = 0.0, S = 0.0;
+    uint32_t tk = 0, wl = 0, wi = 0, G = 0, jc = 0, ew = 0;
+    double t = 0.0, S = 0.0;
+    // the current state as the raw 32-byte Edge slot it was gathered from
+    // ({j, off}, {deg_flags, inv_rate}, d, v)
+    unsigned long long ea = 0, eb = 0, ec = 0, ed = 0;
+#define OFF ((uint32_t)(ea >> 32))
+#define DEGF ((uint32_t)eb)
+#define IR (__uint_as_float((uint32_t)(eb >> 32)))
+#define DCUR (__longlong_as_double((long long)ec))
+#define VCUR (__longlong_as_double((long long)ed))
     // per-task accumulators of the oldest task (lane = jumper index mod 32)
     double s1 = 0.0, s2 = 0.0;
     unsigned long long jsum = 0;
@@ -154,20 +161,20 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     // path ends (park S', v, jumps in the ticket; lane becomes idle) or the
     // grid points are credited and the walker must jump (`jmp`).
     auto sojourn = [&](bool& fin, bool& jmp) {
-        const float h = __fmul_rn(neg_ln_u(ew), ir);
+        const float h = __fmul_rn(neg_ln_u(ew), IR);
         const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
         if (tn >= p.n_grid) {
             // park the raw weight sum; the exponent is formed at accumulation
-            S = __fma_rn(dcur, (double)(p.N + 1 - G), S);
+            S = __fma_rn(DCUR, (double)(p.N + 1 - G), S);
             const uint32_t pos = tk & (CAP - 1);
-            q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, dcur)) : S;
-            q.v[pos] = vcur;
+            q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, DCUR)) : S;
+            q.v[pos] = VCUR;
             q.tk[pos].x = jc;
             act = false;
             fin = true;
         } else {
             const uint32_t kk = (uint32_t)ceil(tn);
-            S = __fma_rn(dcur, (double)(kk - G), S);
+            S = __fma_rn(DCUR, (double)(kk - G), S);
             G = kk;
             t = tn;
             jmp = true;
@@ -281,8 +288,11 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 ew = t2.x;
                 wl = t2.y;
                 const TaskRec& m = q.task[t2.x & 7u];
-                off = m.rr.off; degf = m.rr.deg_flags;
-                ir = m.rr.inv_rate; dcur = m.rr.d; vcur = m.rr.v;
+                const uint4 r0 = *reinterpret_cast<const uint4*>(&m.rr);  // off, degf, ir, T0
+                ea = (unsigned long long)r0.x << 32;
+                eb = r0.y | ((unsigned long long)r0.z << 32);
+                ec = (unsigned long long)__double_as_longlong(m.rr.d);
+                ed = (unsigned long long)__double_as_longlong(m.rr.v);
                 wi = m.i;
                 t = 0.0; S = 0.0; G = 0; jc = 0;
                 act = true;
@@ -315,10 +325,12 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         // ---- C: one jump for every walker whose sojourn did not end the path
         if (jmp) {
             const U4 B = philox4x32_10(U4{jc, wl, wi, kTagEntry}, p.rk);
-            const Edge e = jump_edge(B.y, B.w, B.z, off, degf, adj, thr, alias);
+            const uint32_t off = OFF, degf = DEGF;
+            uint32_t k = pick_index(B.y, B.w, degf & kDegMask);
+            if ((degf & kNonUniform) && B.z >= __ldg(thr + off + k)) k = __ldg(alias + off + k);
+            ld256(adj + off + k, ea, eb, ec, ed);
             ew = B.x;
             ++jc;
-            off = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d; vcur = e.v;
         }
         // ---- accumulate finished tickets in batches of 32 (lane = ticket -
         // tstart mod 32) and finalize completed tasks, oldest first.  The
@@ -399,6 +411,11 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         if (tf == tw && !aopen && atask >= ntask) break;  // every task finalized
     }
 }
+#undef OFF
+#undef DEGF
+#undef IR
+#undef DCUR
+#undef VCUR
 
 // WPR > 1: combine the parts of each row in index order (same tree as the
 // contract: part 0, then += part 1, ...).
