@@ -137,6 +137,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     // newest is being swept while `aopen`
     uint32_t tw = 0, tf = 0;
     bool aopen = false;
+    // register copy of the oldest task's {tend, closed} (ocl false: none or open)
+    uint32_t oend = 0;
+    bool ocl = false;
     uint32_t atask = blockIdx.x * 4u + warp;  // next task to open / the open task
     uint32_t achunk = 0;
     uint32_t head = 0, tail = 0;  // ticket counters (positions mod CAP)
@@ -213,6 +216,10 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             a.K = T0 >= (1ull << 31) ? f0 : 0.0;
             a.corr = p.strang ? __dmul_rn(0.5, ri.d) : ri.d;
         }
+        if (tf == tw) {  // the new task is the oldest in flight
+            ocl = dead;
+            oend = tail;
+        }
         ++tw;
         achunk = part;
         if (dead) {
@@ -258,6 +265,10 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             if (lane == 0) {
                 q.task[sl].tend = tail;
                 q.task[sl].closed = 1u;
+            }
+            if (tw - 1 == tf) {
+                ocl = true;
+                oend = tail;
             }
             aopen = false;
             atask += tstride;
@@ -333,41 +344,41 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             ++jc;
         }
         // ---- accumulate finished tickets in batches of 32 (lane = ticket -
-        // tstart mod 32) and finalize completed tasks, oldest first.  The
-        // condition can only change in an iteration that popped a ticket or
-        // retired a walker.
-        if (!(idle | __ballot_sync(FULL, fin))) continue;
-        __syncwarp();
-        // tickets before `ready` are popped and finished: the oldest ticket
-        // still walking (or the first not popped) bounds it
+        // tstart mod 32) and finalize completed tasks, oldest first.  Tickets
+        // [xc, xc + rdy) are popped and finished: the oldest ticket still
+        // walking (or the first not popped) bounds them.
         const uint32_t minoff = __reduce_min_sync(FULL, act ? tk - xc : ~0u);
-        const uint32_t ready = head - xc < minoff ? head : xc + minoff;
+        uint32_t rdy = head - xc < minoff ? head - xc : minoff;
+        if (rdy < 32u && !(ocl && rdy >= oend - xc)) {
+            if (tf == tw && !aopen && atask >= ntask) break;  // every task finalized
+            continue;
+        }
+        __syncwarp();
         while (tf != tw) {
             const TaskRec& m = q.task[tf & (RT - 1)];
-            const uint2 ec = *reinterpret_cast<const uint2*>(&m.tend);  // {tend, closed}
-            // tickets of this task that are ready
-            const uint32_t lim = ec.y && ec.x - xc < ready - xc ? ec.x : ready;
-            uint32_t be;
-            if (lim - xc >= 32u) {
-                be = xc + 32u;                // a full batch
-            } else if (ec.y && lim == ec.x) {
-                be = lim;                     // the closed task's last (partial) batch
+            // ready tickets of this task (offsets from xc)
+            const uint32_t lim = ocl && oend - xc < rdy ? oend - xc : rdy;
+            uint32_t nb;
+            if (lim >= 32u) {
+                nb = 32u;                     // a full batch
+            } else if (ocl && lim == oend - xc) {
+                nb = lim;                     // the closed task's last (partial) batch
             } else {
                 break;                        // wait for more tickets
             }
-            if (be != xc) {
-                const uint32_t k = xc + lane;
-                if (k < be) {
-                    const uint32_t pos = k & (CAP - 1);
+            if (nb) {
+                if ((uint32_t)lane < nb) {
+                    const uint32_t pos = (xc + lane) & (CAP - 1);
                     const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], m.corr));
                     const double dv = __dsub_rn(__dmul_rn(exp_det(x), q.v[pos]), m.K);
                     s1 = __dadd_rn(s1, dv);
                     s2 = __fma_rn(dv, dv, s2);
                     jsum += q.tk[pos].x;
                 }
-                xc = be;
+                xc += nb;
+                rdy -= nb;
             }
-            if (!ec.y || xc != ec.x) continue;
+            if (!ocl || xc != oend) continue;
             // task complete: butterfly, never-jumpers, output
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -407,6 +418,12 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             jsum = 0;
             ++tf;
             __syncwarp();
+            ocl = false;
+            if (tf != tw) {
+                const uint2 e = *reinterpret_cast<const uint2*>(&q.task[tf & (RT - 1)].tend);
+                ocl = e.y != 0u;
+                oend = e.x;
+            }
         }
         if (tf == tw && !aopen && atask >= ntask) break;  // every task finalized
     }
