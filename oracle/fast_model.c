@@ -137,34 +137,24 @@ void fm_build_records(uint64_t n, const uint64_t* row_ptr, const double* rate,
     }
 }
 
-/* Deviation f - f0 of walker l of row i (0 for walkers that never jump).
- * Word schedule of the kernel: first holding time from the decision word
- * (counter 0xffffffff, 128*(l/128) + l%32, i, tag; word (l%128)/32); jump j
- * from counter (j, l, i, tag): y,w = 64-bit pick, z = alias coin, x = next
- * holding time. */
+/* Deviation f - f0 of jumper l of row i, whose first holding time is
+ * E0 / rate_i (E0 = R of its gap, already < λ).  Jump j draws counter
+ * (j, l, i, tag): y,w = 64-bit pick, z = alias coin, x = next holding time. */
 static double fm_walker(const fm_rec* rec, const uint32_t* nbr, const uint32_t* thr,
-                        const uint32_t* alias, uint32_t i, uint64_t l, uint64_t T0,
-                        double f0, double corr_i, double dt, double inv_dt, double n_grid,
-                        uint64_t N, int strang, uint32_t k0, uint32_t k1,
-                        uint64_t* jumps, int* jumped) {
-    const uint32_t base = (uint32_t)((l / 128) * 128);
-    const uint32_t dctr[4] = {0xffffffffu, base + (uint32_t)(l % 32), i, FM_TAG_ENTRY};
-    uint32_t dw[4];
-    fm_philox(dctr, k0, k1, dw);
-    const uint32_t ew0 = dw[(l % 128) / 32];
-    *jumped = 0;
-    if ((uint64_t)ew0 < T0) return 0.0; /* never jumps: accounted per part */
-    *jumped = 1;
+                        const uint32_t* alias, uint32_t i, uint32_t l, float E0, double f0,
+                        double corr_i, double dt, double inv_dt, double n_grid, uint64_t N,
+                        int strang, uint32_t k0, uint32_t k1, uint64_t* jumps) {
     fm_rec cur = rec[i];
-    uint32_t ew = ew0, g = 0, jc = 0;
+    float E = E0;
+    uint32_t g = 0, jc = 0;
     double t = 0.0, S = 0.0;
     for (;;) {
-        const float h = fm_neg_ln_u(ew) * cur.inv_rate;
+        const float h = E * cur.inv_rate;
         const double tn = t + (double)h * inv_dt;
         if (tn >= n_grid) {
             S = fma(cur.d, (double)(N + 1 - g), S);
             /* the kernel parks S - d_end/2 (Strang) and forms the exponent
-             * at chunk finalize: x = dt * (S' - corr_i) */
+             * at accumulation: x = dt * (S' - corr_i) */
             const double Sp = strang ? S - 0.5 * cur.d : S;
             const double x = dt * (Sp - corr_i);
             *jumps += jc;
@@ -174,7 +164,7 @@ static double fm_walker(const fm_rec* rec, const uint32_t* nbr, const uint32_t* 
         S = fma(cur.d, (double)(kk - g), S);
         g = kk;
         t = tn;
-        const uint32_t ctr[4] = {jc, (uint32_t)l, i, FM_TAG_ENTRY};
+        const uint32_t ctr[4] = {jc, l, i, FM_TAG_ENTRY};
         uint32_t w[4];
         fm_philox(ctr, k0, k1, w);
         uint32_t k = fm_pick(w[1], w[3], cur.degf & FM_DEGMASK);
@@ -182,15 +172,20 @@ static double fm_walker(const fm_rec* rec, const uint32_t* nbr, const uint32_t* 
             if (w[2] >= thr[cur.off + k]) k = alias[cur.off + k];
         }
         cur = rec[nbr[cur.off + k]];
-        ew = w[0];
+        E = fm_neg_ln_u(w[0]);
         ++jc;
     }
 }
 
-/* Accumulation contract of the kernel: part w (of WPR = T/32 parts) owns
- * the walkers l with floor(l/128) = w (mod WPR).  Its jumpers, numbered
- * k = 0, 1, ... in increasing l, are summed by lane k mod 32 in increasing k;
- * xor butterfly over lanes; parts in index order. */
+/* Accumulation contract of the kernel.  Part w (of WPR = T/32 parts) owns
+ * the walkers [floor(wW/WPR), floor((w+1)W/WPR)).  They are decided by a
+ * stream of gap rounds: round r draws Philox counters (0xfffffff0 | w,
+ * 32r + s, i, tag) for s = 0..31, and the 128 words, in order (s, word),
+ * give E = -ln u ~ Exp(1), K = min(floor(E * (1/λ)), 2^27) never-jumpers
+ * and then one jumper with first holding time R/rate, R = max(E - λK, 0)
+ * (fp32, λ = rate β).  The part's jumpers, numbered k = 0, 1, ... in walker
+ * order, are summed by lane k mod 32 in increasing k; xor butterfly over
+ * lanes; parts in index order. */
 void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
                 const uint32_t* thr, const uint32_t* alias, const uint32_t* rows,
                 uint64_t nrows, double beta, uint64_t N, uint64_t W, int strang,
@@ -201,45 +196,58 @@ void fm_entries(const fm_rec* rec, const double* rate, const uint32_t* nbr,
     const double n_grid = (double)N;
     const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
     const uint32_t wpr = T / 32;
-    const uint64_t nch = (W + 127) / 128;
     for (uint64_t r = 0; r < nrows; ++r) {
         const uint32_t i = rows[r];
         const fm_rec ri = rec[i];
-        const double p0 = fm_exp(-(rate[i] * beta));
+        const double lam = rate[i] * beta;
+        const double p0 = fm_exp(-lam);
         const uint64_t T0 = (uint64_t)(p0 * 4294967296.0);
         const double f0 = fm_exp(beta * ri.d) * ri.v;
         /* deviation shift: f0 if never-jumpers are the majority, else 0 */
         const double K = T0 >= (1ull << 31) ? f0 : 0.0;
         const double corr_i = strang ? 0.5 * ri.d : ri.d;
+        const int dead = (T0 >> 32) != 0;
+        const float lamf = (float)lam;
+        const float ilam = dead ? 0.0f : (float)(1.0 / lam);
         double w1 = 0.0, w2 = 0.0;
         uint64_t wj = 0;
         for (uint32_t wi = 0; wi < wpr; ++wi) {
+            const uint32_t L0 = (uint32_t)(W * wi / wpr);
+            const uint32_t nw = (uint32_t)(W * (wi + 1) / wpr) - L0;
             double b1[32], b2[32];
             uint64_t bj[32];
             for (int s = 0; s < 32; ++s) { b1[s] = 0.0; b2[s] = 0.0; bj[s] = 0; }
-            uint32_t n0 = 0; /* never-jumpers of this part */
-            uint64_t nj = 0; /* jumpers of this part so far */
-            for (uint64_t c = wi; c < nch; c += wpr) {
-                for (int q = 0; q < 4; ++q) {
-                    for (int s = 0; s < 32; ++s) {
-                        const uint64_t l = c * 128 + 32 * q + s;
-                        if (l >= W) continue;
-                        uint64_t jl = 0;
-                        int jumped = 0;
-                        const double dev = fm_walker(rec, nbr, thr, alias, i, l, T0, K, corr_i,
-                                                     dt, inv_dt, n_grid, N, strang, k0, k1, &jl,
-                                                     &jumped);
-                        if (!jumped) {
-                            ++n0;
-                            continue; /* exact zero: skipped (bit-identical) */
+            uint64_t nj = 0;  /* jumpers of this part */
+            if (!dead && nw > 0) {
+                uint64_t pos = 0; /* next undecided part-local walker */
+                for (uint32_t round = 0; pos < nw; ++round) {
+                    for (uint32_t s = 0; s < 32 && pos < nw; ++s) {
+                        const uint32_t ctr[4] = {0xfffffff0u | wi, 32u * round + s, i,
+                                                 FM_TAG_ENTRY};
+                        uint32_t wd[4];
+                        fm_philox(ctr, k0, k1, wd);
+                        for (int q = 0; q < 4 && pos < nw; ++q) {
+                            const float E = fm_neg_ln_u(wd[q]);
+                            float kf = floorf(E * ilam);
+                            if (kf > 134217728.0f) kf = 134217728.0f;
+                            float R = fmaf(-lamf, kf, E);
+                            if (R < 0.0f) R = 0.0f;
+                            pos += (uint64_t)kf;
+                            if (pos >= nw) break;
+                            uint64_t jl = 0;
+                            const double dev =
+                                fm_walker(rec, nbr, thr, alias, i, L0 + (uint32_t)pos, R, K,
+                                          corr_i, dt, inv_dt, n_grid, N, strang, k0, k1, &jl);
+                            const int ln = (int)(nj++ % 32);
+                            b1[ln] = b1[ln] + dev;
+                            b2[ln] = fma(dev, dev, b2[ln]);
+                            bj[ln] += jl;
+                            pos += 1;
                         }
-                        const int ln = (int)(nj++ % 32);
-                        b1[ln] = b1[ln] + dev;
-                        b2[ln] = fma(dev, dev, b2[ln]);
-                        bj[ln] += jl;
                     }
                 }
             }
+            const uint32_t n0 = nw - (uint32_t)nj; /* never-jumpers of this part */
             for (int o = 16; o > 0; o >>= 1) {
                 double c1[32], c2[32];
                 uint64_t cj[32];

@@ -473,8 +473,8 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
     } else if (nrows != n) {
         throw InvalidArg("rows == NULL requires nrows == n");
     }
-    if (fast && p->samples >= (1ull << 32))
-        throw InvalidArg("samples must be < 2^32 for the entry walker");
+    if (fast && p->samples >= (1ull << 29))
+        throw InvalidArg("samples must be < 2^29 for the entry walker");
     if (nrows == 0) return;
     DeviceGuard g(h->device);
     cudaStream_t s = h->stream;
@@ -1068,8 +1068,8 @@ int expmc_cuda_entries_device(expmc_matrix* h, const uint32_t* rows_dev, uint64_
         validate_params(p);
         if (p->rng != EXPMC_RNG_PHILOX)
             throw InvalidArg("entries_device supports the Philox walker only");
-        if (p->samples >= (1ull << 32))
-            throw InvalidArg("samples must be < 2^32 for the entry walker");
+        if (p->samples >= (1ull << 29))
+            throw InvalidArg("samples must be < 2^29 for the entry walker");
         if (nrows >= (1ull << 30)) throw InvalidArg("at most 2^30 rows per call");
         DeviceGuard g(h->device);
         // scratch is owned by the handle: one stream per handle at a time

@@ -7,20 +7,24 @@
 //    sojourn; a sojourn in state s over grid time [t, t') credits d_s to every
 //    grid point k Δt inside it, half weights at k = 0 and k = N for Strang
 //    (run_path, estimator.cpp:26-39).  Cost O(1 + jumps) per walker.
-//  * Philox4x32-10 keyed by the seed.  Walker l of row i: its first holding
-//    time comes from a decision word shared 4-per-Philox-block
-//    (counter (0xffffffff, 128c + (l mod 32), i, 'ENTR'), word (l mod 128)/32,
-//    c = l / 128); its j-th jump draws counter (j, l, i, 'ENTR'): words y,w =
-//    64-bit neighbour pick, z = alias coin, x = next holding time.  Randomness
-//    is a pure function of (seed, row, walker).
-//  * Walkers that never jump (decision word < 2^32 e^{-rate_i β}) score the
-//    deterministic f0 = e^{β d_i} v_i; sums are kept as deviations from f0, so
-//    they contribute exact zeros and cost 1/4 of a Philox block.
+//  * Philox4x32-10 keyed by the seed.  Walkers are decided by gaps: part w
+//    of row i owns walkers [wW/WPR, (w+1)W/WPR); gap round r draws counters
+//    (0xfffffff0 | w, 32r + lane, i, 'ENTR'), and each of the 128 words gives
+//    E = -ln u ~ Exp(1) = λK + R (λ = rate_i β): K = ⌊E/λ⌋ walkers that never
+//    jump (Geometric), then one jumper whose first holding time is R/rate_i
+//    (R ~ Exp(1) truncated to [0, λ), independent of K).  Jumper l's j-th
+//    jump draws counter (j, l, i, 'ENTR'): words y,w = 64-bit neighbour pick,
+//    z = alias coin, x = next holding time.  Randomness is a pure function of
+//    (seed, row, part, walker).
+//  * Walkers that never jump score the deterministic f0 = e^{β d_i} v_i; sums
+//    are kept as deviations from a shift K (f0 when never-jumpers dominate),
+//    so they contribute exact zeros, and cost nothing: decisions cost ~1.6
+//    warp instructions per jumper instead of a quarter Philox per walker.
 //  * One dependent 32-B gather per jump through the fat adjacency (Edge).
 //  * Warp-cooperative scheduling over a stream of tasks.  Task t = (row
-//    t / WPR, part t % WPR) owns the row's chunks c ≡ part (mod WPR) of 128
-//    walkers.  A warp sweeps chunks (one Philox block per lane) and appends
-//    the jumpers as tickets to a shared-memory ring of CAP tickets (up to
+//    t / WPR, part t % WPR).  A warp runs gap rounds (one Philox block per
+//    lane, 128 gaps) and appends the jumpers as tickets (first holding time,
+//    walker) to a shared-memory ring of CAP tickets (up to
 //    ENTRY_TASKS tasks in flight); idle lanes pop tickets in order, across
 //    chunk and row boundaries, so the sojourn code runs with (nearly) full
 //    warps.  A finishing walker only parks its raw weight sum S, end value v
@@ -30,8 +34,7 @@
 //    the task on lane k mod 32, straight into that lane's running sums), and
 //    a task is finalized once its last batch is in.
 //  * Fixed accumulation order (result contract, replayed by
-//    oracle/fast_model.c): part w of a row owns the walkers with
-//    floor(l/128) ≡ w (mod WPR); its jumpers, numbered k = 0, 1, ... in
+//    oracle/fast_model.c): the jumpers of part w, numbered k = 0, 1, ... in
 //    increasing l, are summed by lane k mod 32 in increasing k; lanes are
 //    combined by an xor butterfly, parts in index order.  Independent of
 //    scheduling, grid shape, GPU count and row sharding.
@@ -79,12 +82,12 @@ struct RowRecU {     // RowRec without its 32-byte alignment (smem copy)
 // (chunks are admitted task by task), so the accumulation lane of a jumper
 // is its part-local jumper index mod 32 = (ticket - tstart) mod 32.
 struct __align__(16) TaskRec {
-    RowRecU rr;      // record of the start row
+    RowRecU rr;      // record of the start row (rr.spare: 1/λ as fp32 bits)
     uint32_t i;      // matrix row
-    uint32_t nw;     // walkers of the task part
+    uint32_t n0;     // walkers of the task part; once closed: its never-jumpers
     uint32_t tend;   // one past its last ticket (valid once closed)
-    uint32_t closed; // all chunks swept (read with tend as one 8-byte word)
-    uint32_t tstart; // first ticket of the task
+    uint32_t closed; // all walkers decided (read with tend as one 8-byte word)
+    float lam;       // λ = rate_i β (fp32), the never-jump exponent
     uint32_t task;   // task id (row index in the launch, times WPR, plus part)
     double f0;       // e^{β d_i} v_i (score of a walker that never jumps)
     double K;        // shift of the deviation sums: f0 when never-jumpers are the
@@ -99,8 +102,8 @@ struct WarpState {
     double S[CAP];      // per ticket: raw weight sum at finish
     double v[CAP];      // per ticket: v at the end state
     TaskRec task[RT];   // (16-byte aligned: the pop reads rr as one uint4)
-    uint2 tk[CAP + 1];  // per ticket: {decision word (low 3 bits: task slot) until
-                        //   popped, then the jump count; walker index l}; the
+    uint2 tk[CAP + 1];  // per ticket: {first holding time R·rate (fp32) until popped,
+                        //   then the jump count; task slot << 29 | walker l}; the
                         //   last is the sink of the sweep's unconditional stores
                         //   (7 blocks x (smem + 1 KB) must stay under the 196 KB
                         //   carveout: 1 KB more moved config 4 to a 28 KB L1 and
@@ -129,7 +132,6 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     const unsigned lt = (1u << lane) - 1u;
     __shared__ WarpState<RT, CAP> states[4];
     WarpState<RT, CAP>& q = states[warp];
-    const uint32_t nch = (uint32_t)((p.W + kChunk - 1) / kChunk);
     const uint32_t ntask = (uint32_t)(nrows * WPR);
     const uint32_t tstride = gridDim.x * 4u;
 
@@ -141,7 +143,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     uint32_t oend = 0;
     bool ocl = false;
     uint32_t atask = blockIdx.x * 4u + warp;  // next task to open / the open task
-    uint32_t achunk = 0;
+    // the open task's decision cursor: next undecided walker (part-local),
+    // gap round, part walker range [al0, al0 + anw), first ticket
+    uint32_t apos = 0, around = 0, al0 = 0, anw = 0, atstart = 0;
     uint32_t head = 0, tail = 0;  // ticket counters (positions mod CAP)
     uint32_t xc = 0;              // accumulation cursor: tickets before it are summed
     // lane-private walker state
@@ -163,8 +167,8 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     // One sojourn of the lane's walker from its current state: either the
     // path ends (park S', v, jumps in the ticket; lane becomes idle) or the
     // grid points are credited and the walker must jump (`jmp`).
-    auto sojourn = [&](bool& fin, bool& jmp) {
-        const float h = __fmul_rn(neg_ln_u(ew), IR);
+    auto sojourn = [&](float E, bool& fin, bool& jmp) {  // E ~ Exp(1)
+        const float h = __fmul_rn(E, IR);
         const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
         if (tn >= p.n_grid) {
             // park the raw weight sum; the exponent is formed at accumulation
@@ -185,32 +189,30 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     };
 
     // Open task `atask` in slot tw: row constants computed by two lanes in
-    // parallel (lane 0: e^{-rate β}, lane 1: e^{β d}).
+    // parallel (lane 0: e^{-λ}, lane 1: e^{β d}).  Part w of a row owns the
+    // walkers [⌊wW/WPR⌋, ⌊(w+1)W/WPR⌋).
     auto open_task = [&] {
         const int sl = (int)(tw & (RT - 1));
         const uint32_t i = rows[atask / WPR];
         const RowRec ri = load_rec(rec, i);
-        const double rt = __ldg(rate + i);
-        const double ex = exp_det(lane == 0 ? -__dmul_rn(rt, p.beta) : __dmul_rn(p.beta, ri.d));
+        const double lam = __dmul_rn(__ldg(rate + i), p.beta);
+        const double ex = exp_det(lane == 0 ? -lam : __dmul_rn(p.beta, ri.d));
         const double e0 = __shfl_sync(FULL, ex, 0), e1 = __shfl_sync(FULL, ex, 1);
         const unsigned long long T0 = (unsigned long long)__dmul_rn(e0, 4294967296.0);
         const uint32_t part = atask % WPR;
-        const uint32_t ncp = nch > part ? (nch - part + WPR - 1) / WPR : 0u;  // chunks of the part
-        const uint64_t lastb = (uint64_t)(part + (ncp - 1) * WPR) * kChunk;   // its last chunk
-        const uint32_t nw = ncp == 0 ? 0u
-                                      : (ncp - 1) * kChunk +
-                                            (uint32_t)(p.W - lastb < (uint64_t)kChunk ? p.W - lastb
-                                                                                     : kChunk);
-        const bool dead = (T0 >> 32) != 0 || ncp == 0;  // T0 = 2^32: never jumps
+        al0 = (uint32_t)(p.W * part / WPR);
+        anw = (uint32_t)(p.W * (part + 1) / WPR) - al0;
+        const bool dead = (T0 >> 32) != 0 || anw == 0;  // e^{-λ} rounds to 1: never jumps
         if (lane == 0) {
             TaskRec& a = q.task[sl];
-            a.rr = RowRecU{ri.off, ri.deg_flags, ri.inv_rate, (uint32_t)T0, ri.d, ri.v};
+            a.rr = RowRecU{ri.off, ri.deg_flags, ri.inv_rate,
+                           dead ? 0u : __float_as_uint((float)__drcp_rn(lam)), ri.d, ri.v};
             a.i = i;
-            a.nw = nw;
-            a.tstart = tail;
+            a.n0 = anw;
             a.tend = tail;
             a.task = atask;
             a.closed = dead ? 1u : 0u;
+            a.lam = (float)lam;
             const double f0 = __dmul_rn(e1, ri.v);
             a.f0 = f0;
             a.K = T0 >= (1ull << 31) ? f0 : 0.0;
@@ -221,7 +223,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             oend = tail;
         }
         ++tw;
-        achunk = part;
+        apos = 0;
+        around = 0;
+        atstart = tail;
         if (dead) {
             atask += tstride;
         } else {
@@ -230,8 +234,13 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         __syncwarp();
     };
 
-    // Sweep the next chunk of the open task: decide its walkers and append the
-    // jumpers as tickets.
+    // One gap round of the open task: 128 Exp(1) variates E (4 per lane, in
+    // lane-major order) each decide a run of walkers.  E = λK + R with
+    // K = ⌊E/λ⌋ ~ Geometric(1 - e^{-λ}) never-jumpers followed by one jumper
+    // whose first holding time is R/rate, R ~ Exp(1) truncated to [0, λ) and
+    // independent of K (memorylessness) — the law of W independent walkers,
+    // at a cost per jumper instead of per walker.  Jumpers within the part
+    // become tickets, in walker order.
     auto can_admit = [&] {
         return aopen ? tail + kChunk - xc <= CAP : (atask < ntask && tw - tf < (uint32_t)RT);
     };
@@ -242,29 +251,50 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         }
         const uint32_t sl = (tw - 1) & (RT - 1);
         const TaskRec& a = q.task[sl];
-        const uint32_t base = achunk * kChunk;
-        const uint64_t rem = p.W - base;
-        const uint32_t nw = rem < (uint64_t)kChunk ? (uint32_t)rem : (uint32_t)kChunk;
-        const uint32_t T0 = a.rr.spare;
-        const U4 D = philox4x32_10(U4{0xffffffffu, base + (uint32_t)lane, a.i, kTagEntry}, p.rk);
+        const float lamf = a.lam, ilam = __uint_as_float(a.rr.spare);
+        const U4 D = philox4x32_10(
+            U4{0xfffffff0u | (atask % WPR), 32u * around + (uint32_t)lane, a.i, kTagEntry}, p.rk);
         const uint32_t wd[4] = {D.x, D.y, D.z, D.w};
+        uint32_t off[4];
+        float R[4];
+        uint32_t loc = 0;  // walkers decided by this lane's earlier gaps
 #pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-            const uint32_t l = 32u * qq + lane;
-            const bool jmp = l < nw && wd[qq] >= T0;
-            const unsigned b = __ballot_sync(FULL, jmp);
-            // branch-free: non-jumpers store to the sink slot
-            const uint32_t pos = jmp ? ((tail + __popc(b & lt)) & (CAP - 1)) : CAP;
-            q.tk[pos] = make_uint2((wd[qq] & ~7u) | sl, base + l);
-            tail += __popc(b);
+        for (int k = 0; k < 4; ++k) {
+            const float E = neg_ln_u(wd[k]);
+            const float kf = fminf(floorf(__fmul_rn(E, ilam)), 134217728.0f);  // 2^27 cap
+            R[k] = fmaxf(__fmaf_rn(-lamf, kf, E), 0.0f);
+            off[k] = loc + (uint32_t)kf;  // this gap's jumper, lane-relative
+            loc = off[k] + 1u;
         }
-        const uint32_t nextc = achunk + WPR;
-        if (nextc < nch) {
-            achunk = nextc;
-        } else {  // task fully swept
+        // exclusive scan of the lane totals, saturating at 2^31 - 1 (a
+        // saturated prefix still exceeds any part, W < 2^29; no u32 wrap)
+        uint32_t inc = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc = min(inc + y, 0x7fffffffu);
+        }
+        const uint32_t exc = inc - loc;  // exact below the cap
+        const uint32_t total = __shfl_sync(FULL, inc, 31);
+        // jumper positions increase in lane-major order, so the valid ones
+        // are a prefix: ticket (lane, k) goes to tail + 4 lane + k
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t P = apos + exc + off[k];  // part-local walker
+            const bool ok = P < anw;
+            cnt += __popc(__ballot_sync(FULL, ok));
+            const uint32_t pos = ok ? ((tail + 4u * lane + k) & (CAP - 1)) : CAP;
+            q.tk[pos] = make_uint2(__float_as_uint(R[k]), (sl << 29) | (al0 + P));
+        }
+        tail += cnt;
+        apos = min(apos + total, 0x7fffffffu);
+        ++around;
+        if (apos >= anw) {  // every walker of the part decided
             if (lane == 0) {
                 q.task[sl].tend = tail;
                 q.task[sl].closed = 1u;
+                q.task[sl].n0 = anw - (tail - atstart);
             }
             if (tw - 1 == tf) {
                 ocl = true;
@@ -279,7 +309,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     while (true) {
         // ---- A: sojourn of every walker in flight
         bool fin = false, jmp = false;
-        if (act) sojourn(fin, jmp);
+        if (act) sojourn(neg_ln_u(ew), fin, jmp);
         unsigned idle = __ballot_sync(FULL, !act);
         // scheduler work only when enough lanes are free (batching pops
         // amortises the scheduler over several walkers)
@@ -296,10 +326,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             if (!act && rank < take) {
                 tk = head + rank;
                 const uint2 t2 = q.tk[tk & (CAP - 1)];
-                ew = t2.x;
-                wl = t2.y;
-                const TaskRec& m = q.task[t2.x & 7u];
-                const uint4 r0 = *reinterpret_cast<const uint4*>(&m.rr);  // off, degf, ir, T0
+                wl = t2.y & 0x1fffffffu;
+                const TaskRec& m = q.task[t2.y >> 29];
+                const uint4 r0 = *reinterpret_cast<const uint4*>(&m.rr);  // off, degf, ir, -
                 ea = (unsigned long long)r0.x << 32;
                 eb = r0.y | ((unsigned long long)r0.z << 32);
                 ec = (unsigned long long)__double_as_longlong(m.rr.d);
@@ -307,9 +336,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 wi = m.i;
                 t = 0.0; S = 0.0; G = 0; jc = 0;
                 act = true;
-                // a jumper's first sojourn ends in a jump (decision word >= T0),
-                // so it joins this iteration's jump
-                sojourn(fin, jmp);
+                // a jumper's first sojourn (R < λ) ends in a jump, so it joins
+                // this iteration's jump
+                sojourn(__uint_as_float(t2.x), fin, jmp);
             }
             head += take;
 #ifdef ENTRY_STATS
@@ -389,7 +418,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             if (lane == 0) {
                 // never-jumpers score f0: deviation f0 - K each (0 when K = f0)
                 const double f0 = m.f0, K = m.K;
-                const uint32_t n0 = m.nw - (m.tend - m.tstart);
+                const uint32_t n0 = m.n0;
                 const double c = __dsub_rn(f0, K);
                 if (n0 != 0 && c != 0.0) {
                     s1 = __fma_rn((double)n0, c, s1);
