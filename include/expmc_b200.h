@@ -143,10 +143,11 @@ int expmc_cuda_entries_device(expmc_matrix* m, const uint32_t* rows_dev, uint64_
  * listed row (memory-only walker, same access pattern as K3), async. */
 int expmc_cuda_gather_ceiling_device(expmc_matrix* m, const uint32_t* rows_dev, uint64_t nrows,
                                      uint32_t chains_per_row, uint32_t chain_len, void* stream);
-/* Lane slots T per entry used by the Philox entry walker for W walkers:
- * walker l runs in slot l mod T, slots are summed sequentially, then by a
- * fixed xor tree per warp and in warp order — part of the result contract
- * (oracle/fast_model.c replays it). */
+/* Lane slots T per entry used by the Philox entry walker for W walkers
+ * (W < 2^29): the entry's walkers are split into T/32 contiguous parts; the
+ * k-th jumper of a part is summed in lane k mod 32, lanes by a fixed xor
+ * tree, parts in order — part of the result contract (oracle/fast_model.c
+ * replays it). */
 uint32_t expmc_cuda_entry_slots(uint64_t walkers);
 /* Number of kernels this library has launched in this process. */
 uint64_t expmc_cuda_launch_count(void);

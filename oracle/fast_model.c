@@ -77,8 +77,9 @@ float fm_neg_ln_u(uint32_t w) {
 
 /* exp_det of csrc/common.cuh: the kernel's deterministic fp64 exp. */
 double fm_exp(double x) {
-    if (!(x < 709.782712893384)) return x != x ? x : INFINITY;
-    if (x < -745.1332191019412) return 0.0;
+    if (x != x) return x;
+    x = x > 710.0 ? 710.0 : x;
+    x = x < -746.0 ? -746.0 : x;
     const double n = rint(x * 1.4426950408889634);
     double r = fma(-n, 6.93147180369123816490e-01, x);
     r = fma(-n, 1.90821492927058770002e-10, r);
@@ -96,25 +97,14 @@ double fm_exp(double x) {
     q = fma(q, r, 0.5);
     q = fma(q, r, 1.0);
     q = fma(q, r, 1.0);
-    const long long k = (long long)n;
-    uint64_t b;
-    double s;
-    if (k > 1023) {
-        b = (uint64_t)2046 << 52;
-        memcpy(&s, &b, 8);
-        return (q * 2.0) * s;
-    }
-    if (k >= -1022) {
-        b = (uint64_t)(k + 1023) << 52;
-        memcpy(&s, &b, 8);
-        return q * s;
-    }
-    b = (uint64_t)(k + 1023 + 54) << 52;
-    memcpy(&s, &b, 8);
-    double t;
-    uint64_t b2 = (uint64_t)(1023 - 54) << 52;
-    memcpy(&t, &b2, 8);
-    return (q * s) * t;
+    /* 2^k as 2^k1 * 2^k2: exact until the last rounding (csrc/common.cuh) */
+    const int k = (int)n;
+    const int k1 = k >> 1, k2 = k - k1;
+    uint64_t b1 = (uint64_t)(k1 + 1023) << 52, b2 = (uint64_t)(k2 + 1023) << 52;
+    double s1, s2;
+    memcpy(&s1, &b1, 8);
+    memcpy(&s2, &b2, 8);
+    return (q * s1) * s2;
 }
 
 static uint32_t fm_pick(uint32_t hi, uint32_t lo, uint32_t n) {

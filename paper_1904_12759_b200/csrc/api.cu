@@ -128,6 +128,7 @@ FastParams fast_params(const expmc_path_params* p, uint64_t walkers) {
     f.dt = p->beta / (double)p->n_steps;  // PathParams::dt, estimator.hpp:27
     f.inv_dt = 1.0 / f.dt;
     f.n_grid = (double)p->n_steps;
+    f.n_grid1 = (double)p->n_steps + 1.0;
     f.N = (uint32_t)p->n_steps;
     f.strang = p->splitting == EXPMC_STRANG;
     f.W = walkers;

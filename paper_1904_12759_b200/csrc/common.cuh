@@ -164,7 +164,7 @@ __device__ __forceinline__ float neg_ln_u(uint32_t w) {
 // e^x in fp64 from IEEE-exact operations only (rint, fma, mul), so the CPU
 // model (oracle/fast_model.c fm_exp) reproduces it bit for bit: Cody-Waite
 // reduction x = n ln2 + r, |r| <= ln2/2, degree-13 Taylor for e^r, exact
-// scaling by 2^n.  Max error ~1 ulp on [-745, 709.78].
+// scaling by 2^n.  Max error ~1 ulp on [-745, 709.78]; +inf above, 0 below.
 // Coefficients as immediates (UMOV pairs).  Measured: 2% faster on K3 than
 // reading them from the constant bank (-DEXP_DET_CONST, kept as a variant).
 #ifndef EXP_DET_CONST
@@ -193,8 +193,13 @@ __constant__ double c_exp_det[16] = {
     1.6666666666666665741e-01, 709.782712893384, -745.1332191019412};
 
 __device__ __forceinline__ double exp_det(double x) {
-    if (!(x < EXPC(14))) return x != x ? x : __longlong_as_double(0x7ff0000000000000LL);
-    if (x < EXPC(15)) return 0.0;
+    // branch-free range handling: clamp (NaN passes through: the compares
+    // are false), then scale by 2^k as 2^k1 * 2^k2 (k1 = k >> 1), which is
+    // exact up to the final rounding for every k in [-1076, 1024]: the same
+    // value as one correctly rounded q * 2^k, including overflow to +inf
+    // (x >= ln(DBL_MAX)) and underflow to subnormals / 0
+    x = x > 710.0 ? 710.0 : x;
+    x = x < -746.0 ? -746.0 : x;
     const double n = rint(__dmul_rn(x, EXPC(0)));
     double r = __fma_rn(-n, EXPC(1), x);
     r = __fma_rn(-n, EXPC(2), r);
@@ -204,13 +209,10 @@ __device__ __forceinline__ double exp_det(double x) {
     q = __fma_rn(q, r, 0.5);
     q = __fma_rn(q, r, 1.0);
     q = __fma_rn(q, r, 1.0);
-    const long long k = (long long)n;
-    if (k > 1023)  // 2^1024 is not representable: q * 2 * 2^1023
-        return __dmul_rn(__dmul_rn(q, 2.0), __longlong_as_double(2046LL << 52));
-    if (k >= -1022)
-        return __dmul_rn(q, __longlong_as_double((k + 1023) << 52));
-    return __dmul_rn(__dmul_rn(q, __longlong_as_double((k + 1023 + 54) << 52)),
-                     __longlong_as_double((long long)(1023 - 54) << 52));
+    const int k = __double2int_rn(n);
+    const int k1 = k >> 1;
+    return __dmul_rn(__dmul_rn(q, __longlong_as_double((long long)(k1 + 1023) << 52)),
+                     __longlong_as_double((long long)(k - k1 + 1023) << 52));
 }
 
 // floor(x * n / 2^64) for a 64-bit uniform x: unbiased to n / 2^64.

@@ -38,6 +38,7 @@ struct FastParams {
     double dt;     // β / N
     double inv_dt; // N / β
     double n_grid; // (double) N
+    double n_grid1; // (double) (N + 1)
     uint32_t N;
     int strang;
     uint64_t W;    // walkers per entry (K3) or total walkers (K4)

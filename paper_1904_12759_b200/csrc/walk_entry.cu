@@ -150,8 +150,10 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     uint32_t xc = 0;              // accumulation cursor: tickets before it are summed
     // lane-private walker state
     bool act = false;
-    uint32_t tk = 0, wl = 0, wi = 0, G = 0, jc = 0, ew = 0;
-    double t = 0.0, S = 0.0;
+    uint32_t tk = 0, wl = 0, wi = 0, jc = 0, ew = 0;
+    // G: grid points credited so far, kept as an exact integer-valued double
+    // (ceil in fp64, no int conversions on the XU pipe)
+    double t = 0.0, S = 0.0, G = 0.0;
     // the current state as the raw 32-byte Edge slot it was gathered from
     // ({j, off}, {deg_flags, inv_rate}, d, v)
     unsigned long long ea = 0, eb = 0, ec = 0, ed = 0;
@@ -172,7 +174,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
         if (tn >= p.n_grid) {
             // park the raw weight sum; the exponent is formed at accumulation
-            S = __fma_rn(DCUR, (double)(p.N + 1 - G), S);
+            S = __fma_rn(DCUR, __dsub_rn(p.n_grid1, G), S);
             const uint32_t pos = tk & (CAP - 1);
             q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, DCUR)) : S;
             q.v[pos] = VCUR;
@@ -180,8 +182,8 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             act = false;
             fin = true;
         } else {
-            const uint32_t kk = (uint32_t)ceil(tn);
-            S = __fma_rn(DCUR, (double)(kk - G), S);
+            const double kk = ceil(tn);
+            S = __fma_rn(DCUR, __dsub_rn(kk, G), S);
             G = kk;
             t = tn;
             jmp = true;
@@ -334,7 +336,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 ec = (unsigned long long)__double_as_longlong(m.rr.d);
                 ed = (unsigned long long)__double_as_longlong(m.rr.v);
                 wi = m.i;
-                t = 0.0; S = 0.0; G = 0; jc = 0;
+                t = 0.0; S = 0.0; G = 0.0; jc = 0;
                 act = true;
                 // a jumper's first sojourn (R < λ) ends in a jump, so it joins
                 // this iteration's jump

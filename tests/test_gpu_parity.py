@@ -461,3 +461,30 @@ def test_vector_estimate_is_bitwise_deterministic(pb, graphs, rng):
         assert np.array_equal(a.values, b.values)
         assert a.std_error_global == b.std_error_global and a.total_jumps == b.total_jumps
         assert np.all(a.values >= 0.0)  # v >= 0 -> nonnegative
+
+
+@pytest.mark.parametrize("W", [1, 2, 127, 129, 4097, 10007])
+def test_philox_walker_gap_edge_cases(pb, orc, graphs, W):
+    """Gap decisions at the edges: parts of unequal size (W not a multiple of
+    the part count), single-walker entries, sparse jumpers (tiny β: gaps of
+    thousands of walkers), rows whose walkers all jump, and dead rows
+    (e^{-λ} rounds to 1) — bit-exact against the CPU model."""
+    csr = graphs["fd2d_16"]
+    m = pb.split(csr)
+    s = orc.split(csr)
+    v = pb.gen_vector(1, csr.n, 9)
+    rows = np.arange(0, csr.n, 17, dtype=np.uint32)
+    for beta in (1e-12, 1e-5, 0.05, 3.0):
+        p = pb.PathParams(beta, 32, W, pb.Splitting.Strang, 5, pb.Rng.PHILOX)
+        got = pb.entries_estimate(m, v, rows, p)
+        mv, ms, mj = orc.fast_entries(s, v, rows, beta, 32, W, 0, 5, pb.entry_slots(W))
+        assert np.array_equal(got.values, mv), (beta, np.max(np.abs(got.values - mv)))
+        assert np.array_equal(got.std_errors, ms), beta
+        assert np.array_equal(got.jumps, mj), beta
+
+
+def test_entry_walker_sample_limit(pb, graphs):
+    m = pb.split(graphs["p3"])
+    p = pb.PathParams(1.0, 8, 1 << 29, pb.Splitting.Strang, 1, pb.Rng.PHILOX)
+    with pytest.raises(ValueError, match="samples must be < 2\\^29 for the entry walker"):
+        pb.entries_estimate(m, np.ones(3), np.array([0], np.uint32), p)

@@ -205,3 +205,23 @@ def test_model_jump_count_matches_rate(orc):
     _, _, j = orc.fast_entries(s, np.ones(500), rows, 1.5, 32, 5000, 1, 3, 32)
     per_path = j.sum() / (len(rows) * 5000)
     assert abs(per_path - 1.5 * 4) / 6.0 < 0.05
+
+
+@pytest.mark.parametrize("lam", [1e-4, 0.02, 0.3, 2.0, 12.0])
+def test_model_gap_decisions_poisson_law(orc, lam):
+    """Gap decisions (E = λK + R) keep the per-walker law: on a 2-regular
+    ring every state has rate 2, so a walker's jump count is Poisson(2β).
+    Covers sparse jumpers (λ = 1e-4: gaps of ~1e4 walkers), the regime of
+    the headline config (λ ~ 0.3) and walkers that all jump (λ = 12)."""
+    import paper_1904_12759_b200 as pb
+
+    csr = pb.gen_ws(64, 1, 0.0, 1)  # ring: every row degree 2, weight 1
+    s = orc.split(csr)
+    assert np.all(s["rate"] == 2.0)
+    beta = lam / 2.0
+    rows = np.arange(0, 64, 8, dtype=np.uint32)
+    W = 20011  # parts of unequal size (WPR = 4)
+    _, _, j = orc.fast_entries(s, np.ones(64), rows, beta, 32, W, 1, 5, pb.entry_slots(W))
+    n = len(rows) * W
+    mean, sd = n * lam, math.sqrt(n * lam)
+    assert abs(float(j.sum()) - mean) < 5 * sd + 1, (float(j.sum()), mean)
