@@ -70,7 +70,7 @@ class Oracle:
     """ctypes view of liboracle.so."""
 
     def __init__(self):
-        L = _load(os.path.join(HERE, "liboracle.so"))
+        L = _load(os.environ.get("EXPMC_ORACLE_LIB") or os.path.join(HERE, "liboracle.so"))
         self.L = L
         L.orc_rng_draws.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p]
         L.orc_split.argtypes = [C.c_uint64, _u64p, _u32p, _f64p, _f64p, _f64p, _f64p, _f64p,

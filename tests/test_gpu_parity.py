@@ -477,7 +477,8 @@ def test_philox_walker_gap_edge_cases(pb, orc, graphs, W):
     for beta in (1e-12, 1e-5, 0.05, 3.0):
         p = pb.PathParams(beta, 32, W, pb.Splitting.Strang, 5, pb.Rng.PHILOX)
         got = pb.entries_estimate(m, v, rows, p)
-        mv, ms, mj = orc.fast_entries(s, v, rows, beta, 32, W, 0, 5, pb.entry_slots(W))
+        mv, ms, mj = orc.fast_entries(s, v, rows, beta, 32, W, int(pb.Splitting.Strang), 5,
+                                      pb.entry_slots(W))
         assert np.array_equal(got.values, mv), (beta, np.max(np.abs(got.values - mv)))
         assert np.array_equal(got.std_errors, ms), beta
         assert np.array_equal(got.jumps, mj), beta
