@@ -507,7 +507,7 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
         CK(cudaMemsetAsync(sc, 0, 16, s));
         launch_count_nonfinite(n, vd, flag, s);
         launch_pack_v(n, vd, h->m.rec, s);
-        launch_pack_v_adj(h->m.nnz, vd, h->m.adj, s);
+        launch_pack_v_adj(h->m.nnz, h->m.neighbor, vd, h->m.adj, s);
         after_launch(3);
         mark(s);
         if (nrows >= (1ull << 30)) throw InvalidArg("at most 2^30 rows per call");
@@ -1056,7 +1056,7 @@ int expmc_cuda_set_v_device(expmc_matrix* h, const double* v_dev, uint64_t nv, v
         CK(cudaStreamSynchronize(s));
         if (bad) throw InvalidArg("non-finite entry in v");
         launch_pack_v(nv, v_dev, h->m.rec, s);
-        launch_pack_v_adj(h->m.nnz, v_dev, h->m.adj, s);
+        launch_pack_v_adj(h->m.nnz, h->m.neighbor, v_dev, h->m.adj, s);
         after_launch(2);
     });
 }

@@ -63,7 +63,8 @@ void launch_alias_build(uint64_t n, const uint64_t* row_ptr, const double* weigh
 void launch_pack_v(uint64_t n, const double* v, RowRec* rec, cudaStream_t s);
 void launch_build_adj(uint64_t nnz, const uint32_t* neighbor, const RowRec* rec, Edge* adj,
                       cudaStream_t s);
-void launch_pack_v_adj(uint64_t nnz, const double* v, Edge* adj, cudaStream_t s);
+void launch_pack_v_adj(uint64_t nnz, const uint32_t* neighbor, const double* v, Edge* adj,
+                       cudaStream_t s);
 void launch_node_factors(uint64_t n, const double* d, double scale, double* f,
                          cudaStream_t s);
 

@@ -168,11 +168,14 @@ __global__ void build_adj_kernel(uint64_t nnz, const uint32_t* __restrict__ neig
 
 // Per call: refresh v_j in every fat-adjacency slot (8-B stores at a 32-B
 // stride, gathers of v from an L2-resident vector).
-__global__ void pack_v_adj_kernel(uint64_t nnz, const double* __restrict__ v,
-                                  Edge* __restrict__ adj) {
+// Per-call refresh of Edge.v: the landing row comes from the 4-byte CSR
+// neighbour array (0.64 GB at config 5) rather than from the 32-byte slots
+// themselves (5.1 GB), so the pass reads 8x less.
+__global__ void pack_v_adj_kernel(uint64_t nnz, const uint32_t* __restrict__ neighbor,
+                                  const double* __restrict__ v, Edge* __restrict__ adj) {
     const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (e >= nnz) return;
-    adj[e].v = __ldg(v + adj[e].j);
+    adj[e].v = __ldg(v + __ldg(neighbor + e));
 }
 
 void launch_build_adj(uint64_t nnz, const uint32_t* neighbor, const RowRec* rec, Edge* adj,
@@ -181,9 +184,10 @@ void launch_build_adj(uint64_t nnz, const uint32_t* neighbor, const RowRec* rec,
     build_adj_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(nnz, neighbor, rec, adj);
 }
 
-void launch_pack_v_adj(uint64_t nnz, const double* v, Edge* adj, cudaStream_t s) {
+void launch_pack_v_adj(uint64_t nnz, const uint32_t* neighbor, const double* v, Edge* adj,
+                       cudaStream_t s) {
     if (nnz == 0) return;
-    pack_v_adj_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(nnz, v, adj);
+    pack_v_adj_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(nnz, neighbor, v, adj);
 }
 
 __global__ void pack_v_kernel(uint64_t n, const double* __restrict__ v, RowRec* __restrict__ rec) {

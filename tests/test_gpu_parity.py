@@ -326,6 +326,16 @@ def test_device_api_matches_host_api(pb, graphs):
     assert np.array_equal(val.cpu().numpy(), host.values)
     assert np.array_equal(se.cpu().numpy(), host.std_errors)
     assert np.array_equal(jm.cpu().numpy().astype(np.uint64), host.jumps)
+    # a newly staged v is what the walkers read (the per-call layout is
+    # refreshed): doubling v doubles every value and SE exactly
+    vd2 = vd * 2.0
+    pb.set_v_device(m, vd2.data_ptr(), csr.n, stream)
+    pb.entries_device(m, rows.data_ptr(), csr.n, p, val.data_ptr(), se.data_ptr(),
+                      jm.data_ptr(), stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(val.cpu().numpy(), 2.0 * host.values)
+    assert np.array_equal(se.cpu().numpy(), 2.0 * host.std_errors)
+    assert np.array_equal(jm.cpu().numpy().astype(np.uint64), host.jumps)
 
 
 def test_results_invariant_to_row_sharding(pb, graphs):
