@@ -120,9 +120,7 @@ __global__ void __launch_bounds__(128, ENTRY_MIN_BLOCKS)
 entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rate,
                   const Edge* __restrict__ adj, const uint32_t* __restrict__ thr,
                   const uint32_t* __restrict__ alias, const uint32_t* __restrict__ rows,
-                  uint64_t nrows, FastParams p, double* __restrict__ out_value,
-                  double* __restrict__ out_se, uint64_t* __restrict__ out_jumps,
-                  double4* __restrict__ partial) {
+                  uint64_t nrows, FastParams p, double4* __restrict__ partial) {
     constexpr int RT = ENTRY_TASKS;
     constexpr uint32_t CAP = ENTRY_CAP;
     static_assert((RT & (RT - 1)) == 0 && RT <= 8 && (CAP & (CAP - 1)) == 0 && CAP >= kChunk,
@@ -426,23 +424,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                     s1 = __fma_rn((double)n0, c, s1);
                     s2 = __fma_rn((double)n0, __dmul_rn(c, c), s2);
                 }
-                const uint64_t task = m.task;
-                if (WPR == 1) {
-                    const double W = (double)p.W;
-                    out_value[task] = __dadd_rn(K, __ddiv_rn(s1, W));
-                    double se = 0.0;
-                    if (p.W > 1) {
-                        double var = __ddiv_rn(__dsub_rn(s2, __ddiv_rn(__dmul_rn(s1, s1), W)),
-                                               __dsub_rn(W, 1.0));
-                        var = var > 0.0 ? var : 0.0;
-                        se = sqrt(__ddiv_rn(var, W));
-                    }
-                    out_se[task] = se;
-                    out_jumps[task] = jsum;
-                } else {
-                    partial[task] =
-                        make_double4(s1, s2, __longlong_as_double((long long)jsum), K);
-                }
+                // the divisions and sqrt of the estimate run in the
+                // row-parallel combine pass, not on one lane here
+                partial[m.task] = make_double4(s1, s2, __longlong_as_double((long long)jsum), K);
             }
             s1 = 0.0;
             s2 = 0.0;
@@ -465,8 +449,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
 #undef DCUR
 #undef VCUR
 
-// WPR > 1: combine the parts of each row in index order (same tree as the
-// contract: part 0, then += part 1, ...).
+// Combine the parts of each row in index order (same tree as the contract:
+// part 0, then += part 1, ...) and form the estimate: mean K + Σdev / W,
+// SE from the one-pass variance clamped at 0 (finalize, estimator.cpp:76-89).
 template <int WPR>
 __global__ void combine_parts_kernel(const double4* __restrict__ partial, uint64_t nrows,
                                      uint64_t W, double* __restrict__ out_value,
@@ -552,13 +537,10 @@ int launch_t(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const Fast
     const uint64_t cap = (uint64_t)nsm * ENTRY_MIN_BLOCKS;
     const unsigned grid = (unsigned)(blocks < cap ? blocks : cap);
     entry_walk_kernel<WPR><<<grid, 128, pad, s>>>(m.rec, m.rate, m.adj, m.alias_thr, m.alias_idx,
-                                                rows, nrows, p, value, se, jumps, partial);
-    if (WPR > 1) {
-        combine_parts_kernel<WPR><<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(
-            partial, nrows, p.W, value, se, jumps);
-        return 2;
-    }
-    return 1;
+                                                rows, nrows, p, partial);
+    combine_parts_kernel<WPR><<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(
+        partial, nrows, p.W, value, se, jumps);
+    return 2;
 }
 
 }  // namespace
@@ -570,8 +552,7 @@ int entry_fast_wpr(uint64_t W) {
 }
 
 size_t entry_fast_scratch_bytes(uint64_t nrows, uint64_t W) {
-    const int wpr = entry_fast_wpr(W);
-    return wpr > 1 ? nrows * (size_t)wpr * sizeof(double4) : 0;
+    return nrows * (size_t)entry_fast_wpr(W) * sizeof(double4);
 }
 
 int launch_entry_fast(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
