@@ -161,57 +161,69 @@ __device__ __forceinline__ float neg_ln_u(uint32_t w) {
     return -ln_u;
 }
 
-// e^x in fp64 from IEEE-exact operations only (rint, fma, mul), so the CPU
-// model (oracle/fast_model.c fm_exp) reproduces it bit for bit: Cody-Waite
-// reduction x = n ln2 + r, |r| <= ln2/2, degree-13 Taylor for e^r, exact
-// scaling by 2^n.  Max error ~1 ulp on [-745, 709.78]; +inf above, 0 below.
-// Coefficients as immediates (UMOV pairs).  Measured: 2% faster on K3 than
-// reading them from the constant bank (-DEXP_DET_CONST, kept as a variant).
-#ifndef EXP_DET_CONST
-#define EXPC(k) (exp_det_lit(k))
-__device__ __forceinline__ constexpr double exp_det_lit(int k) {
-    return k == 0 ? 1.4426950408889634 : k == 1 ? 6.93147180369123816490e-01
-         : k == 2 ? 1.90821492927058770002e-10 : k == 3 ? 1.6059043836821614599e-10
-         : k == 4 ? 2.0876756987868098979e-09 : k == 5 ? 2.5052108385441718775e-08
-         : k == 6 ? 2.7557319223985890653e-07 : k == 7 ? 2.7557319223985890653e-06
-         : k == 8 ? 2.4801587301587301566e-05 : k == 9 ? 1.9841269841269841253e-04
-         : k == 10 ? 1.3888888888888889419e-03 : k == 11 ? 8.3333333333333332177e-03
-         : k == 12 ? 4.1666666666666664354e-02 : k == 13 ? 1.6666666666666665741e-01
-         : k == 14 ? 709.782712893384 : -745.1332191019412;
-}
-#else
-#define EXPC(k) (c_exp_det[k])
-#endif
-__constant__ double c_exp_det[16] = {
-    1.4426950408889634,         // log2(e)
-    6.93147180369123816490e-01, // ln2 hi
-    1.90821492927058770002e-10, // ln2 lo
-    1.6059043836821614599e-10,  // 1/13!
-    2.0876756987868098979e-09, 2.5052108385441718775e-08, 2.7557319223985890653e-07,
-    2.7557319223985890653e-06, 2.4801587301587301566e-05, 1.9841269841269841253e-04,
-    1.3888888888888889419e-03, 8.3333333333333332177e-03, 4.1666666666666664354e-02,
-    1.6666666666666665741e-01, 709.782712893384, -745.1332191019412};
+// e^x in fp64 from IEEE-exact operations only (rint, fma, mul, add), so the
+// CPU model (oracle/fast_model.c fm_exp) reproduces it bit for bit.
+// Table-driven: x = (32k + j) ln2/32 + r, |r| <= ln2/64; e^x = 2^k 2^(j/32)
+// e^r with 2^(j/32) as a double-double {hi, lo} (32 entries, 512 B, L1
+// resident) and e^r - 1 = r(1 + r/2 + ... + r^5/720) (truncation 3e-18):
+// y = hi + fma(hi, e^r - 1, lo), ~0.5 ulp.  Six dependent DFMAs instead of
+// a degree-13 chain.  Range handling is branch-free: x is clamped (NaN
+// passes through: the compares are false) and 2^k applied as 2^k1 * 2^k2,
+// exact up to the final rounding, so overflow gives +inf and underflow
+// rounds to subnormals / 0 like a single correctly rounded scaling.
+__device__ const double2 kExpTab[32] = {
+    {0x1.0000000000000p+0, 0x0.0p+0},
+    {0x1.059b0d3158574p+0, 0x1.d73e2a475b465p-55},
+    {0x1.0b5586cf9890fp+0, 0x1.8a62e4adc610bp-54},
+    {0x1.11301d0125b51p+0, -0x1.6c51039449b3ap-54},
+    {0x1.172b83c7d517bp+0, -0x1.19041b9d78a76p-55},
+    {0x1.1d4873168b9aap+0, 0x1.e016e00a2643cp-54},
+    {0x1.2387a6e756238p+0, 0x1.9b07eb6c70573p-54},
+    {0x1.29e9df51fdee1p+0, 0x1.612e8afad1255p-55},
+    {0x1.306fe0a31b715p+0, 0x1.6f46ad23182e4p-55},
+    {0x1.371a7373aa9cbp+0, -0x1.63aeabf42eae2p-54},
+    {0x1.3dea64c123422p+0, 0x1.ada0911f09ebcp-55},
+    {0x1.44e086061892dp+0, 0x1.89b7a04ef80d0p-59},
+    {0x1.4bfdad5362a27p+0, 0x1.d4397afec42e2p-56},
+    {0x1.5342b569d4f82p+0, -0x1.07abe1db13cadp-55},
+    {0x1.5ab07dd485429p+0, 0x1.6324c054647adp-54},
+    {0x1.6247eb03a5585p+0, -0x1.383c17e40b497p-54},
+    {0x1.6a09e667f3bcdp+0, -0x1.bdd3413b26456p-54},
+    {0x1.71f75e8ec5f74p+0, -0x1.16e4786887a99p-55},
+    {0x1.7a11473eb0187p+0, -0x1.41577ee04992fp-55},
+    {0x1.82589994cce13p+0, -0x1.d4c1dd41532d8p-54},
+    {0x1.8ace5422aa0dbp+0, 0x1.6e9f156864b27p-54},
+    {0x1.93737b0cdc5e5p+0, -0x1.75fc781b57ebcp-57},
+    {0x1.9c49182a3f090p+0, 0x1.c7c46b071f2bep-56},
+    {0x1.a5503b23e255dp+0, -0x1.d2f6edb8d41e1p-54},
+    {0x1.ae89f995ad3adp+0, 0x1.7a1cd345dcc81p-54},
+    {0x1.b7f76f2fb5e47p+0, -0x1.5584f7e54ac3bp-56},
+    {0x1.c199bdd85529cp+0, 0x1.11065895048ddp-55},
+    {0x1.cb720dcef9069p+0, 0x1.503cbd1e949dbp-56},
+    {0x1.d5818dcfba487p+0, 0x1.2ed02d75b3707p-55},
+    {0x1.dfc97337b9b5fp+0, -0x1.1a5cd4f184b5cp-54},
+    {0x1.ea4afa2a490dap+0, -0x1.e9c23179c2893p-54},
+    {0x1.f50765b6e4540p+0, 0x1.9d3e12dd8a18bp-54}};
 
 __device__ __forceinline__ double exp_det(double x) {
-    // branch-free range handling: clamp (NaN passes through: the compares
-    // are false), then scale by 2^k as 2^k1 * 2^k2 (k1 = k >> 1), which is
-    // exact up to the final rounding for every k in [-1076, 1024]: the same
-    // value as one correctly rounded q * 2^k, including overflow to +inf
-    // (x >= ln(DBL_MAX)) and underflow to subnormals / 0
     x = x > 710.0 ? 710.0 : x;
     x = x < -746.0 ? -746.0 : x;
-    const double n = rint(__dmul_rn(x, EXPC(0)));
-    double r = __fma_rn(-n, EXPC(1), x);
-    r = __fma_rn(-n, EXPC(2), r);
-    double q = EXPC(3);
-#pragma unroll
-    for (int k = 4; k < 14; ++k) q = __fma_rn(q, r, EXPC(k));
-    q = __fma_rn(q, r, 0.5);
-    q = __fma_rn(q, r, 1.0);
-    q = __fma_rn(q, r, 1.0);
-    const int k = __double2int_rn(n);
+    const double n = rint(__dmul_rn(x, 0x1.71547652b82fep+5));  // 32 / ln2
+    double r = __fma_rn(-n, 0x1.62e42fee00000p-6, x);  // ln2/32, hi part (exact n*hi)
+    r = __fma_rn(-n, 0x1.a39ef35793c76p-38, r);         // ln2/32, lo part
+    double p = 1.0 / 720.0;
+    p = __fma_rn(p, r, 1.0 / 120.0);
+    p = __fma_rn(p, r, 1.0 / 24.0);
+    p = __fma_rn(p, r, 1.0 / 6.0);
+    p = __fma_rn(p, r, 0.5);
+    p = __fma_rn(p, r, 1.0);
+    p = __dmul_rn(p, r);  // e^r - 1
+    const int ni = __double2int_rn(n);
+    const double2 t = __ldg(&kExpTab[ni & 31]);
+    const double y = __dadd_rn(t.x, __fma_rn(t.x, p, t.y));
+    const int k = ni >> 5;
     const int k1 = k >> 1;
-    return __dmul_rn(__dmul_rn(q, __longlong_as_double((long long)(k1 + 1023) << 52)),
+    return __dmul_rn(__dmul_rn(y, __longlong_as_double((long long)(k1 + 1023) << 52)),
                      __longlong_as_double((long long)(k - k1 + 1023) << 52));
 }
 
