@@ -48,7 +48,7 @@ namespace expmc_b200 {
 
 namespace {
 
-constexpr int kChunk = 128;
+constexpr int kRound = 128;  // gaps per warp round (4 per lane): at most kRound tickets
 constexpr unsigned FULL = 0xffffffffu;
 
 #ifndef ENTRY_MIN_BLOCKS
@@ -59,9 +59,6 @@ constexpr unsigned FULL = 0xffffffffu;
 #endif
 #ifndef ENTRY_CAP
 #define ENTRY_CAP 256   // jumper tickets in flight per warp (power of 2, >= 128)
-#endif
-#ifndef ENTRY_PREFETCH
-#define ENTRY_PREFETCH 0  // tickets kept queued after each jump (0: off; 16-64 measured 2-3% slower)
 #endif
 #ifndef ENTRY_CARVE
 #define ENTRY_CARVE 1     // size the smem carveout for ENTRY_MIN_BLOCKS (max L1)
@@ -123,7 +120,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                   uint64_t nrows, FastParams p, double4* __restrict__ partial) {
     constexpr int RT = ENTRY_TASKS;
     constexpr uint32_t CAP = ENTRY_CAP;
-    static_assert((RT & (RT - 1)) == 0 && RT <= 8 && (CAP & (CAP - 1)) == 0 && CAP >= kChunk,
+    static_assert((RT & (RT - 1)) == 0 && RT <= 8 && (CAP & (CAP - 1)) == 0 && CAP >= kRound,
                   "ring sizes");
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -242,7 +239,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     // at a cost per jumper instead of per walker.  Jumpers within the part
     // become tickets, in walker order.
     auto can_admit = [&] {
-        return aopen ? tail + kChunk - xc <= CAP : (atask < ntask && tw - tf < (uint32_t)RT);
+        return aopen ? tail + kRound - xc <= CAP : (atask < ntask && tw - tf < (uint32_t)RT);
     };
     auto admit = [&] {
         if (!aopen) {
@@ -547,7 +544,7 @@ int launch_t(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const Fast
 
 // Warps (parts) per row: a function of W only (part of the result contract).
 int entry_fast_wpr(uint64_t W) {
-    const uint64_t nch = (W + kChunk - 1) / kChunk;
+    const uint64_t nch = (W + kRound - 1) / kRound;
     return nch >= 64 ? 4 : (nch >= 32 ? 2 : 1);
 }
 
