@@ -152,6 +152,17 @@ uint32_t expmc_cuda_entry_slots(uint64_t walkers);
 /* Number of kernels this library has launched in this process. */
 uint64_t expmc_cuda_launch_count(void);
 
+/* ------------------------------------------- K4 sampler diagnostics (tests) */
+/* `count` draws of the device Binomial(trials, p) sampler used by the
+ * Theorem-2 walkers (inversion / BTRS), Philox-keyed by seed, into out[]. */
+int expmc_cuda_binomial_samples(int device, uint64_t trials, double p, uint64_t count,
+                                uint64_t seed, uint64_t* out);
+/* The K4 start counts: walkers per start row ~ Multinomial(samples, v / V)
+ * (v == NULL: uniform over rows), as vector_estimate / tc_estimate draw them
+ * for (samples, seed).  counts[] has n entries and sums to samples. */
+int expmc_cuda_start_counts(expmc_matrix* m, const double* v, uint64_t nv, uint64_t samples,
+                            uint64_t seed, uint64_t* counts);
+
 /* ------------------------------------------------------- accuracy (K5) */
 /* Deterministic fp64 y = exp(t A) v by scaled Taylor series (tol relative). */
 int expmc_cuda_expmv(expmc_matrix* m, const double* v, uint64_t nv, double t, double tol,

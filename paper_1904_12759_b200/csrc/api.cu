@@ -148,7 +148,7 @@ struct expmc_matrix {
     DevSplit m;
     std::vector<void*> owned;
     DevBuf vdev, rows, out_val, out_se, out_j, fa, vcum, values, pa, pb, pc, scal, tmp1, tmp2,
-        tmp3, iota, part, fa2, sort_tmp, lens;
+        tmp3, iota, part, fa2, sort_tmp, lens, cnt, jcnt, joff, row_of, scan_tmp, rowc;
     uint64_t iota_n = 0;
     // host copies kept for K5 norm bounds
     std::vector<double> h_rate, h_diag;
@@ -163,7 +163,8 @@ struct expmc_matrix {
     ~expmc_matrix() {
         for (void* p : owned) cudaFree(p);
         for (DevBuf* b : {&vdev, &rows, &out_val, &out_se, &out_j, &fa, &vcum, &values, &pa,
-                          &pb, &pc, &scal, &tmp1, &tmp2, &tmp3, &iota, &part, &fa2, &sort_tmp, &lens})
+                          &pb, &pc, &scal, &tmp1, &tmp2, &tmp3, &iota, &part, &fa2, &sort_tmp, &lens, &cnt, &jcnt,
+                          &joff, &row_of, &scan_tmp, &rowc})
             b->release();
         if (stream) cudaStreamDestroy(stream);
         if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -603,6 +604,94 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
     }
 }
 
+// K4 (Philox): Theorem-2 walkers grouped by start row (walk_vec.cu).
+// Multinomial start counts -> per-row never-jumpers (scored in place) and
+// jumper counts -> exclusive scan -> jumper walks in batches, whose (end, f)
+// records go through the deterministic sort-based per-end reduction.
+// Tallies: row partials, then batch partials, added on the host in order.
+void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_path_params* p,
+                 double* vals, double* values_host, double* sum_out, double* sq_out,
+                 uint64_t* jumps_out) {
+    cudaStream_t s = h->stream;
+    const uint64_t n = h->m.n, M = p->samples;
+    const FastParams fp = fast_params(p, M);
+    uint64_t* cnt = h->cnt.get<uint64_t>(n);
+    uint64_t* jc = h->jcnt.get<uint64_t>(n + 1);
+    uint64_t* off = h->joff.get<uint64_t>(n + 1);
+    const int levels = launch_start_counts(n, M, vcum, fp.rk, cnt, s);
+    after_launch(levels);
+    const unsigned rparts = vec_rows_grid(), wparts = vec_walk_grid();
+    const unsigned parts = std::max(rparts, wparts);
+    double* pa = h->pa.get<double>(parts);
+    double* pb = h->pb.get<double>(parts);
+    unsigned long long* pc = h->pc.get<unsigned long long>(parts);
+    double* tot = h->scal.get<double>(4);
+    double2* rowc = h->rowc.get<double2>(n);
+    launch_vec_rows(h->m, cnt, fp, v_sum, vals, jc, rowc, pa, pb, s);
+    CK(cudaMemsetAsync(jc + n, 0, 8, s));
+    CK(cudaMemsetAsync(pc, 0, rparts * sizeof(unsigned long long), s));
+    launch_final_reduce(pa, pb, pc, rparts, tot, tot + 1,
+                        reinterpret_cast<unsigned long long*>(tot + 2), s);
+    const size_t scan_bytes = scan_u64_temp_bytes(n + 1);
+    void* scan_tmp = h->scan_tmp.get<unsigned char>(scan_bytes);
+    launch_scan_u64(jc, off, n + 1, scan_tmp, scan_bytes, s);
+    after_launch(3);
+    double res[3];
+    uint64_t J = 0;
+    CK(cudaMemcpyAsync(res, tot, sizeof(res), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&J, off + n, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double sum = res[0], sq = res[1];
+    uint64_t jumps = 0;
+    // batch buffers sized by M (>= J), not by the random J, so repeated calls
+    // with the same M never regrow (and re-allocate) them
+    const uint64_t B = std::min<uint64_t>(M, 1ull << 26);
+    uint32_t* row_of = h->row_of.get<uint32_t>(B);
+    uint32_t *rec_end = nullptr, *end_sorted = nullptr;
+    double *rec_f = nullptr, *f_sorted = nullptr;
+    void* temp = nullptr;
+    size_t temp_bytes = 0;
+    if (vals) {
+        rec_end = h->tmp1.get<uint32_t>(B * 2);
+        end_sorted = rec_end + B;
+        rec_f = h->tmp2.get<double>(B * 2);
+        f_sorted = rec_f + B;
+        temp_bytes = scatter_sort_temp_bytes(B, n);
+        temp = h->sort_tmp.get<unsigned char>(temp_bytes);
+    }
+    for (uint64_t q0 = 0; q0 < J; q0 += B) {
+        const uint64_t q1 = std::min(J, q0 + B);
+        launch_expand_rows(off, n, q0, q1, row_of, s);
+        launch_vec_walk(h->m, rowc, row_of, off, fp, v_sum, q0, q1, rec_end, rec_f, pa, pb, pc, s);
+        launch_final_reduce(pa, pb, pc, wparts, tot, tot + 1,
+                            reinterpret_cast<unsigned long long*>(tot + 2), s);
+        after_launch(3);
+        if (vals) {
+            scatter_sort_accumulate(rec_end, rec_f, end_sorted, f_sorted, q1 - q0, n, temp,
+                                    temp_bytes, vals, s);
+            after_launch(3);
+            CK(cudaGetLastError());
+        }
+        CK(cudaMemcpyAsync(res, tot, sizeof(res), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        uint64_t j;
+        std::memcpy(&j, &res[2], 8);
+        sum += res[0];
+        sq += res[1];
+        jumps += j;
+    }
+    CK(cudaGetLastError());
+    if (vals) {
+        launch_scale(n, vals, 1.0 / (double)M, s);
+        after_launch(1);
+        CK(cudaMemcpyAsync(values_host, vals, n * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    *sum_out = sum;
+    *sq_out = sq;
+    *jumps_out = jumps;
+}
+
 // Theorem 2 walkers (vector / tc).  start_mode 0 uniform, 1 categorical.
 void run_scatter(expmc_matrix* h, int start_mode, const std::vector<double>* cum, double v_sum,
                  const expmc_path_params* p, double* values_host, double* sum_out,
@@ -621,27 +710,26 @@ void run_scatter(expmc_matrix* h, int start_mode, const std::vector<double>* cum
         CK(cudaMemcpyAsync(c, cum->data(), n * 8, cudaMemcpyHostToDevice, s));
         vc = c;
     }
-    const unsigned parts =
-        p->rng == EXPMC_RNG_PHILOX ? scatter_fast_grid() : scatter_compat_grid();
+    if (p->rng == EXPMC_RNG_PHILOX) {
+        run_grouped(h, vc, v_sum, p, vals, values_host, sum_out, sq_out, jumps_out);
+        return;
+    }
+    const unsigned parts = scatter_compat_grid();
     double* pa = h->pa.get<double>(parts);
     double* pb = h->pb.get<double>(parts);
     unsigned long long* pc = h->pc.get<unsigned long long>(parts);
     const double dt = p->beta / (double)p->n_steps;
     const bool strang = p->splitting == EXPMC_STRANG;
-    double* fac = nullptr;
-    if (p->rng != EXPMC_RNG_PHILOX) {
-        fac = h->fa.get<double>(n);
-        launch_node_factors(n, h->m.d, strang ? dt / 2.0 : dt, fac, s);
-        after_launch(1);
-    }
+    double* fac = h->fa.get<double>(n);
+    launch_node_factors(n, h->m.d, strang ? dt / 2.0 : dt, fac, s);
+    after_launch(1);
     // walkers in batches; per batch: (end, f) records -> stable sort by end
-    // -> reduce-by-key -> values[] += run sums (deterministic, no atomics);
+    // -> per-run sequential sums added to values[] (deterministic, no atomics);
     // scalar tallies reduced per batch and added on the host in batch order
     const uint64_t M = p->samples;
     const uint64_t B = vals ? std::min<uint64_t>(M, 1ull << 25) : M;
-    uint32_t *rec_end = nullptr, *end_sorted = nullptr, *run_keys = nullptr;
-    double *rec_f = nullptr, *f_sorted = nullptr, *run_sums = nullptr;
-    int* nruns = nullptr;
+    uint32_t *rec_end = nullptr, *end_sorted = nullptr;
+    double *rec_f = nullptr, *f_sorted = nullptr;
     void* temp = nullptr;
     size_t temp_bytes = 0;
     if (vals) {
@@ -649,34 +737,25 @@ void run_scatter(expmc_matrix* h, int start_mode, const std::vector<double>* cum
         end_sorted = rec_end + B;
         rec_f = h->tmp2.get<double>(B * 2);
         f_sorted = rec_f + B;
-        run_keys = h->tmp3.get<uint32_t>(B + 2);
-        nruns = h->lens.get<int>(2 * (B + 1) + 2);
-        run_sums = h->fa2.get<double>(B);
         temp_bytes = scatter_sort_temp_bytes(B, n);
         temp = h->sort_tmp.get<unsigned char>(temp_bytes);
     }
-    const FastParams fp = fast_params(p, M);
     double* tot = h->scal.get<double>(4);
     double sum = 0.0, sq = 0.0;
     uint64_t jumps = 0;
     for (uint64_t l0 = 0; l0 < M; l0 += B) {
         const uint64_t lend = std::min(M, l0 + B);
-        if (p->rng == EXPMC_RNG_PHILOX) {
-            launch_scatter_fast(h->m, start_mode, vc, v_sum, fp, l0, lend, rec_end, rec_f, pa, pb,
-                                pc, s);
-        } else {
-            // Lie weight on the state each segment leaves from (estimator.cpp:228-231)
-            launch_scatter_compat(h->m, start_mode, vc, v_sum, dt, p->n_steps, M, fac,
-                                  strang ? fac : nullptr, p->seed, l0, lend, rec_end, rec_f, pa,
-                                  pb, pc, s);
-        }
+        // Lie weight on the state each segment leaves from (estimator.cpp:228-231)
+        launch_scatter_compat(h->m, start_mode, vc, v_sum, dt, p->n_steps, M, fac,
+                              strang ? fac : nullptr, p->seed, l0, lend, rec_end, rec_f, pa, pb,
+                              pc, s);
         launch_final_reduce(pa, pb, pc, parts, tot, tot + 1,
                             reinterpret_cast<unsigned long long*>(tot + 2), s);
         after_launch(2);
         if (vals) {
-            scatter_sort_accumulate(rec_end, rec_f, end_sorted, f_sorted, lend - l0, n, run_keys,
-                                    run_sums, nruns, temp, temp_bytes, vals, s);
-            after_launch(1);
+            scatter_sort_accumulate(rec_end, rec_f, end_sorted, f_sorted, lend - l0, n, temp,
+                                    temp_bytes, vals, s);
+            after_launch(3);
             CK(cudaGetLastError());
         }
         double res[3];
@@ -1079,6 +1158,66 @@ int expmc_cuda_entries_device(expmc_matrix* h, const uint32_t* rows_dev, uint64_
                                         value_dev, std_error_dev, jumps_dev, scratch,
                                         pick_stream(h, stream));
         after_launch(k);
+    });
+}
+
+int expmc_cuda_binomial_samples(int device, uint64_t trials, double p, uint64_t count,
+                                uint64_t seed, uint64_t* out) {
+    return guarded([&] {
+        if (!out && count) throw InvalidArg("out is null");
+        if (!(p >= 0.0 && p <= 1.0)) throw InvalidArg("p must be in [0, 1]");
+        DeviceGuard g(device);
+        uint64_t* d = nullptr;
+        CK(cudaMalloc(&d, (count ? count : 1) * 8));
+        launch_binomial_debug(trials, p, count,
+                              philox_keys((uint32_t)seed, (uint32_t)(seed >> 32)), d, 0);
+        after_launch(count ? 1 : 0);
+        const cudaError_t e = cudaMemcpy(out, d, count * 8, cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        CK(e);
+    });
+}
+
+int expmc_cuda_start_counts(expmc_matrix* h, const double* v, uint64_t nv, uint64_t samples,
+                            uint64_t seed, uint64_t* counts) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        if (!counts) throw InvalidArg("counts is null");
+        DeviceGuard g(h->device);
+        cudaStream_t s = h->stream;
+        const uint64_t n = h->m.n;
+        if (n == 0) throw InvalidArg("empty matrix");
+        const double* vc = nullptr;
+        if (v) {
+            check_vector(h, v, nv);
+            std::vector<double> cum(n);
+            double acc = 0.0;
+            for (uint64_t k = 0; k < n; ++k) {
+                if (v[k] < 0.0) throw InvalidArg("vector_estimate requires v >= 0 entrywise");
+                acc += v[k];
+                cum[k] = acc;
+            }
+            if (!(acc > 0.0)) throw InvalidArg("vector_estimate requires sum(v) > 0");
+            bool uniform = true;  // StartSampler's exact uniform test (estimator.cpp:95-100)
+            for (uint64_t k = 0; k < n; ++k)
+                if (v[k] != v[0]) { uniform = false; break; }
+            if (uniform) v = nullptr;
+        }
+        if (v) {
+            std::vector<double> cum(n);
+            double acc = 0.0;
+            for (uint64_t k = 0; k < n; ++k) { acc += v[k]; cum[k] = acc; }
+            double* c = h->vcum.get<double>(n);
+            CK(cudaMemcpyAsync(c, cum.data(), n * 8, cudaMemcpyHostToDevice, s));
+            CK(cudaStreamSynchronize(s));
+            vc = c;
+        }
+        uint64_t* cnt = h->cnt.get<uint64_t>(n);
+        after_launch(launch_start_counts(n, samples, vc,
+                                         philox_keys((uint32_t)seed, (uint32_t)(seed >> 32)),
+                                         cnt, s));
+        CK(cudaMemcpyAsync(counts, cnt, n * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
     });
 }
 

@@ -97,26 +97,42 @@ double isim_device(const uint32_t* ox_host, const uint32_t* oy_host, uint64_t n,
 
 // scatter_sort.cu
 size_t scatter_sort_temp_bytes(uint64_t batch, uint64_t n);
+// sort + per-run sums; launches 3 kernels (sort counted as one)
 void scatter_sort_accumulate(uint32_t* end, double* f, uint32_t* end_sorted, double* f_sorted,
-                             uint64_t count, uint64_t n, uint32_t* run_keys, double* run_sums,
-                             int* nruns, void* temp, size_t temp_bytes, double* values,
-                             cudaStream_t s);
+                             uint64_t count, uint64_t n, void* temp, size_t temp_bytes,
+                             double* values, cudaStream_t s);
 
-// walk_fast.cu (K3, K4, K6)
+// walk_entry.cu (K3), walk_fast.cu (K6)
 int entry_fast_wpr(uint64_t W);
 size_t entry_fast_scratch_bytes(uint64_t nrows, uint64_t W);
 // returns the number of kernels launched
 int launch_entry_fast(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
                       const FastParams& p, double* value, double* se, uint64_t* jumps,
                       void* scratch, cudaStream_t s);
-unsigned scatter_fast_grid();
-void launch_scatter_fast(const DevSplit& m, int start_mode, const double* vcum, double v_sum,
-                         const FastParams& p, uint64_t l0, uint64_t lend, uint32_t* out_end,
-                         double* out_f, double* part_s1, double* part_s2,
-                         unsigned long long* part_j, cudaStream_t s);
 void launch_gather_ceiling(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
                            uint32_t chains_per_row, uint32_t chain_len, uint32_t salt,
                            unsigned long long* sink, cudaStream_t s);
+
+// walk_vec.cu (K4: vector / tc by grouped starts)
+unsigned vec_rows_grid();
+unsigned vec_walk_grid();
+// returns the number of kernels launched (tree levels)
+int launch_start_counts(uint64_t n, uint64_t M, const double* cum, const PhiloxKeys& K,
+                        uint64_t* cnt, cudaStream_t s);
+void launch_vec_rows(const DevSplit& m, const uint64_t* cnt, const FastParams& p, double v_sum,
+                     double* values, uint64_t* jcount, double2* rowc, double* part_s1,
+                     double* part_s2, cudaStream_t s);
+size_t scan_u64_temp_bytes(uint64_t count);
+void launch_scan_u64(const uint64_t* in, uint64_t* out, uint64_t count, void* temp,
+                     size_t temp_bytes, cudaStream_t s);
+void launch_expand_rows(const uint64_t* off, uint64_t n, uint64_t q0, uint64_t q1,
+                        uint32_t* row_of, cudaStream_t s);
+void launch_vec_walk(const DevSplit& m, const double2* rowc, const uint32_t* row_of, const uint64_t* off,
+                     const FastParams& p, double v_sum, uint64_t q0, uint64_t q1,
+                     uint32_t* out_end, double* out_f, double* part_s1, double* part_s2,
+                     unsigned long long* part_j, cudaStream_t s);
+void launch_binomial_debug(uint64_t n, double p, uint64_t count, const PhiloxKeys& K,
+                           uint64_t* out, cudaStream_t s);
 
 // reduce.cu
 void launch_final_reduce(const double* part_a, const double* part_b,

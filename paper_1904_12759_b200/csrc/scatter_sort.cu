@@ -1,17 +1,18 @@
 // Deterministic per-end-state accumulation for the Theorem-2 estimators
 // (vector_estimate, proj/src/estimator.cpp:250 `local_values[out.end] += f`).
 //
-// The walkers of a batch emit (end, f) records indexed by walker; a stable
-// radix sort by end keeps walker order inside each end state; run-length
-// encoding (integer) + an exclusive scan of the run lengths give each end
-// state's segment, and a segmented reduction sums every segment with one
-// fixed-shape block reduction (no decoupled look-back: ReduceByKey's
-// cross-tile prefix combination order depends on timing and is not bitwise
-// reproducible for doubles).  Run sums are added to values[] in batch order.
+// The walkers of a batch emit (end, f) records in a fixed order (walker /
+// jumper index); a stable radix sort by end keeps that order inside each end
+// state.  Every run is then summed in that order in fixed 32-record pieces
+// (pass A: pieces, runs inside one piece added at once; pass B: runs that
+// cross piece boundaries, pieces added in order) and added to values[end].
+// Each run is added by exactly one thread, so there are no atomics; batches
+// are applied in order, so the result is bitwise reproducible.  (CUB's
+// ReduceByKey combines tile prefixes in a timing-dependent order, which is
+// not bitwise reproducible for doubles.)
+#include <stdexcept>
+
 #include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_run_length_encode.cuh>
-#include <cub/device/device_scan.cuh>
-#include <cub/device/device_segmented_reduce.cuh>
 
 #include "kernels.cuh"
 
@@ -19,10 +20,54 @@ namespace expmc_b200 {
 
 namespace {
 
-__global__ void add_runs_kernel(const uint32_t* __restrict__ keys, const double* __restrict__ sums,
-                                int nruns, double* __restrict__ values) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < nruns) values[keys[k]] = __dadd_rn(values[keys[k]], sums[k]);
+constexpr uint32_t kChunk = 32;  // records per thread in the run-sum passes
+
+// Pass A: thread k owns chunk [kC, kC + C) of the sorted records and sums
+// every run piece in it sequentially.  A run that starts and ends in the
+// chunk is added to values[] here; the piece of a run that started earlier
+// goes to head[k]; the piece of a run that starts here and continues past
+// the chunk goes to tail[k] (completed in pass B).
+__global__ void run_pieces_kernel(const uint32_t* __restrict__ keys, const double* __restrict__ f,
+                                  uint64_t count, double* __restrict__ head,
+                                  double* __restrict__ tail, double* __restrict__ values) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t lo = k * kChunk;
+    if (lo >= count) return;
+    const uint64_t hi = lo + kChunk < count ? lo + kChunk : count;
+    uint64_t pos = lo;
+    while (pos < hi) {
+        const uint32_t key = keys[pos];
+        const bool started = pos > lo || lo == 0 || keys[lo - 1] != key;
+        double s = f[pos];
+        uint64_t j = pos + 1;
+        while (j < hi && keys[j] == key) s = __dadd_rn(s, f[j++]);
+        const bool ends = j < hi || hi == count || keys[hi] != key;
+        if (!started) head[k] = s;
+        else if (ends) values[key] = __dadd_rn(values[key], s);
+        else tail[k] = s;
+        pos = j;
+    }
+}
+
+// Pass B: thread k completes the run that starts in its chunk and crosses
+// its end: tail[k] + head[k+1] + head[k+2] + ... in chunk order.
+__global__ void run_spans_kernel(const uint32_t* __restrict__ keys, uint64_t count,
+                                 const double* __restrict__ head,
+                                 const double* __restrict__ tail, double* __restrict__ values) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t lo = k * kChunk, hi = lo + kChunk;
+    if (hi >= count) return;  // the last chunk has nothing past its end
+    const uint32_t key = keys[hi - 1];
+    if (keys[hi] != key) return;  // no run crosses the end of this chunk
+    // the crossing run started here unless it also covers this chunk's start
+    if (keys[lo] == key && (lo > 0 && keys[lo - 1] == key)) return;
+    double s = tail[k];
+    for (uint64_t c = k + 1; c * kChunk < count && keys[c * kChunk] == key; ++c) {
+        s = __dadd_rn(s, head[c]);
+        const uint64_t e = (c + 1) * kChunk;
+        if (e >= count || keys[e] != key) break;
+    }
+    values[key] = __dadd_rn(values[key], s);
 }
 
 int key_bits(uint64_t n) {
@@ -34,47 +79,33 @@ int key_bits(uint64_t n) {
 }  // namespace
 
 size_t scatter_sort_temp_bytes(uint64_t batch, uint64_t n) {
-    size_t a = 0, b = 0, c = 0, d = 0;
-    const int nb = (int)batch;
+    size_t a = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                    (const double*)nullptr, (double*)nullptr, nb, 0,
+                                    (const double*)nullptr, (double*)nullptr, (int)batch, 0,
                                     key_bits(n));
-    cub::DeviceRunLengthEncode::Encode(nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                       (int*)nullptr, (int*)nullptr, nb);
-    cub::DeviceScan::ExclusiveSum(nullptr, c, (const int*)nullptr, (int*)nullptr, nb + 1);
-    cub::DeviceSegmentedReduce::Sum(nullptr, d, (const double*)nullptr, (double*)nullptr, nb,
-                                    (const int*)nullptr, (const int*)nullptr);
-    size_t m = a;
-    for (size_t x : {b, c, d}) m = x > m ? x : m;
-    return m + 256;
+    const uint64_t chunks = (batch + kChunk - 1) / kChunk;
+    return a + 256 + 2 * chunks * sizeof(double) + 256;
 }
 
-// run_keys / run_sums: `count` entries; run_len / run_off: count + 1 ints
-// (laid out in `lens`, 2 * (count + 1) ints).
 void scatter_sort_accumulate(uint32_t* end, double* f, uint32_t* end_sorted, double* f_sorted,
-                             uint64_t count, uint64_t n, uint32_t* run_keys, double* run_sums,
-                             int* lens, void* temp, size_t temp_bytes, double* values,
-                             cudaStream_t s) {
+                             uint64_t count, uint64_t n, void* temp, size_t temp_bytes,
+                             double* values, cudaStream_t s) {
     if (count == 0) return;
-    const int nb = (int)count;
-    int* run_len = lens;
-    int* run_off = lens + count + 1;
-    int* nruns_d = run_off + count + 1;
-    size_t tb = temp_bytes;
-    cub::DeviceRadixSort::SortPairs(temp, tb, end, end_sorted, f, f_sorted, nb, 0, key_bits(n),
-                                    s);
-    tb = temp_bytes;
-    cub::DeviceRunLengthEncode::Encode(temp, tb, end_sorted, run_keys, run_len, nruns_d, nb, s);
-    int nruns = 0;
-    cudaMemcpyAsync(&nruns, nruns_d, sizeof(int), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    cudaMemsetAsync(run_len + nruns, 0, sizeof(int), s);
-    tb = temp_bytes;
-    cub::DeviceScan::ExclusiveSum(temp, tb, run_len, run_off, nruns + 1, s);
-    tb = temp_bytes;
-    cub::DeviceSegmentedReduce::Sum(temp, tb, f_sorted, run_sums, nruns, run_off, run_off + 1, s);
-    add_runs_kernel<<<(unsigned)((nruns + 255) / 256), 256, 0, s>>>(run_keys, run_sums, nruns,
-                                                                   values);
+    size_t tb = 0;  // the sort's own share of temp (the piece buffers follow it)
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, end, end_sorted, f, f_sorted, (int)count, 0,
+                                    key_bits(n));
+    if (tb + 512 + 2 * ((count + kChunk - 1) / kChunk) * sizeof(double) > temp_bytes)
+        throw std::runtime_error("scatter_sort: temp storage too small");
+    cub::DeviceRadixSort::SortPairs(temp, tb, end, end_sorted, f, f_sorted, (int)count, 0,
+                                    key_bits(n), s);
+    // piece buffers after the sort's temp storage
+    const uint64_t chunks = (count + kChunk - 1) / kChunk;
+    const size_t sort_bytes = (tb + 255) & ~(size_t)255;
+    double* head = reinterpret_cast<double*>(static_cast<unsigned char*>(temp) + sort_bytes);
+    double* tail = head + chunks;
+    const unsigned blocks = (unsigned)((chunks + 255) / 256);
+    run_pieces_kernel<<<blocks, 256, 0, s>>>(end_sorted, f_sorted, count, head, tail, values);
+    run_spans_kernel<<<blocks, 256, 0, s>>>(end_sorted, count, head, tail, values);
 }
 
 }  // namespace expmc_b200

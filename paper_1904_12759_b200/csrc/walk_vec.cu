@@ -1,0 +1,402 @@
+// K4 — Theorem-2 estimators (vector_estimate, proj/src/estimator.cpp:208-278;
+// tc_estimate, :280-318) by grouped starts.
+//
+// The reference draws M i.i.d. walkers, each with its own start
+// (StartSampler, estimator.cpp:92-128: v / V by upper_bound on the
+// cumulative table, or uniform), and sums f = V w over them.  Both outputs —
+// values[j] = (1/M) Σ_{end = j} f and the tallies Σf, Σf², Σjumps — are
+// symmetric functions of the multiset of walkers, so the walkers may be
+// generated in any order with the same joint law.  This file generates
+// them grouped by start row:
+//
+//   1. start counts (c_0..c_{n-1}) ~ Multinomial(M, v / V), drawn down a
+//      binary tree over the row range: a node [lo, hi) holding c walkers
+//      sends Binomial(c, V[lo,mid) / V[lo,hi)) of them left.  Masses are
+//      differences of the reference's own cumulative table, so the leaf
+//      probabilities telescope to exactly the (cum[i] - cum[i-1]) / V the
+//      reference's upper_bound samples;
+//   2. per row, the never-jumpers n0 ~ Binomial(c_i, e^{-λ_i}) (λ_i = rate_i β:
+//      a walker stays put iff its first holding time exceeds β) score the
+//      deterministic f0 = V e^{β d_i} at their own row — added to values[i]
+//      directly, no scatter;
+//   3. the c_i - n0 jumpers, numbered k = 0, 1, ... inside their row, start
+//      with a first holding time R / rate_i, R ~ Exp(1) truncated to [0, λ_i)
+//      (memorylessness), and continue as the continuous-clock walkers of K3;
+//      consecutive lanes walk jumpers of the same row, so the first gathers
+//      share L1 lines.  Their (end, f) records go through the deterministic
+//      sort-based per-end reduction (scatter_sort.cu).
+//
+// Every draw is keyed by position (tree node, row, jumper index within its
+// row), never by thread, and every floating-point sum has a fixed order, so
+// results are bitwise reproducible.
+#include <cub/device/device_scan.cuh>
+
+#include "kernels.cuh"
+
+namespace expmc_b200 {
+
+namespace {
+
+constexpr uint32_t kTagTree = 0x4d554c54u;   // 'MULT' multinomial tree
+constexpr uint32_t kTagStay = 0x53544159u;   // 'STAY' never-jumper binomial
+constexpr uint32_t kTagDebug = 0x44454247u;  // 'DEBG' binomial test hook
+constexpr int kRowsThreads = 256;
+constexpr unsigned kRowsBlocks = 148 * 8;
+
+__device__ __forceinline__ double u53(uint32_t hi, uint32_t lo) {
+    return __dmul_rn((double)((((uint64_t)hi << 32) | lo) >> 11), 0x1.0p-53);
+}
+
+// Stirling remainder fc(k) = ln k! - (k + 1/2) ln(k + 1) + (k + 1) - ln √(2π).
+__device__ __forceinline__ double stirling_tail(double k) {
+    if (k <= 9.0) {
+        // exact values for small k (ln k! by lgamma of an integer is exact to ~1 ulp)
+        return lgamma(k + 1.0) - (k + 0.5) * log(k + 1.0) + (k + 1.0) -
+               0.91893853320467274178;
+    }
+    const double kp1 = k + 1.0, kp1sq = kp1 * kp1;
+    return (1.0 / 12.0 - (1.0 / 360.0 - 1.0 / 1260.0 / kp1sq) / kp1sq) / kp1;
+}
+
+// Binomial(n, p) from the Philox stream (iteration r, id0, id1, tag), one
+// Philox block per iteration.  n * min(p, 1-p) < 10: inversion (sequential
+// pmf search, expected n p + 1 steps); otherwise Hörmann's BTRS
+// (transformed rejection with squeeze, W. Hörmann, "The generation of
+// binomial random variates", J. Stat. Comput. Simul. 46, 1993), exact
+// acceptance test on the Stirling-expanded log pmf ratio.
+__device__ uint64_t binomial(uint64_t n, double p, uint32_t id0, uint32_t id1, uint32_t tag,
+                             const PhiloxKeys& K) {
+    if (n == 0 || !(p > 0.0)) return 0;
+    if (p >= 1.0) return n;
+    const bool flip = p > 0.5;
+    const double pp = flip ? 1.0 - p : p;
+    const double nd = (double)n;
+    uint64_t x = 0;
+    if (nd * pp < 10.0) {
+        const double q = 1.0 - pp, s = pp / q, a = (nd + 1.0) * s;
+        const double r0 = exp(nd * log1p(-pp));
+        for (uint32_t it = 0;; ++it) {
+            const U4 w = philox4x32_10(U4{it, id0, id1, tag}, K);
+            double u = u53(w.x, w.y), r = r0;
+            uint64_t k = 0;
+            bool ok = true;
+            while (u > r) {
+                u -= r;
+                ++k;
+                if (k > n || k > 2000) { ok = false; break; }  // rounding tail: redraw
+                r *= a / (double)k - s;
+            }
+            if (ok) { x = k; break; }
+        }
+    } else {
+        const double spq = sqrt(nd * pp * (1.0 - pp));
+        const double b = 1.15 + 2.53 * spq;
+        const double a = -0.0873 + 0.0248 * b + 0.01 * pp;
+        const double c = nd * pp + 0.5;
+        const double vr = 0.92 - 4.2 / b;
+        const double r = pp / (1.0 - pp);
+        const double alpha = (2.83 + 5.1 / b) * spq;
+        const double m = floor((nd + 1.0) * pp);
+        const double fm = stirling_tail(m) + stirling_tail(nd - m);
+        for (uint32_t it = 0;; ++it) {
+            const U4 w = philox4x32_10(U4{it, id0, id1, tag}, K);
+            const double U = u53(w.x, w.y) - 0.5;
+            const double V = u53(w.z, w.w);
+            const double us = 0.5 - fabs(U);
+            const double kf = floor((2.0 * a / us + b) * U + c);
+            if (kf < 0.0 || kf > nd) continue;
+            if (us >= 0.07 && V <= vr) { x = (uint64_t)kf; break; }
+            const double lv = log(V * alpha / (a / (us * us) + b));
+            const double h = (m + 0.5) * log((m + 1.0) / (r * (nd - m + 1.0))) +
+                             (nd + 1.0) * log1p((kf - m) / (nd - kf + 1.0)) +
+                             (kf + 0.5) * log(r * (nd - kf + 1.0) / (kf + 1.0)) + fm -
+                             stirling_tail(kf) - stirling_tail(nd - kf);
+            if (lv <= h) { x = (uint64_t)kf; break; }
+        }
+    }
+    return flip ? n - x : x;
+}
+
+// One level of the multinomial tree.  Node k of level L covers rows
+// [k << (D-L), (k+1) << (D-L)) ∩ [0, n); its count lives at cnt[lo] and its
+// right child's at cnt[mid] (zero until written here).
+__global__ void tree_level_kernel(uint64_t* __restrict__ cnt, uint64_t n, int D, int L,
+                                  const double* __restrict__ cum, PhiloxKeys K) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= (1ull << L)) return;
+    const uint64_t span = 1ull << (D - L);
+    const uint64_t lo = k * span, mid = lo + span / 2;
+    if (mid >= n) return;  // no right child: the left keeps everything
+    const uint64_t c = cnt[lo];
+    if (c == 0) return;
+    const uint64_t hi = lo + span < n ? lo + span : n;
+    double pl;
+    if (cum) {
+        const double base = lo ? cum[lo - 1] : 0.0;
+        const double left = __dsub_rn(cum[mid - 1], base);
+        const double all = __dsub_rn(cum[hi - 1], base);
+        pl = all > 0.0 ? left / all : 0.5;
+    } else {
+        pl = (double)(mid - lo) / (double)(hi - lo);
+    }
+    const uint64_t x = binomial(c, pl, (uint32_t)k, (uint32_t)L, kTagTree, K);
+    cnt[lo] = x;
+    cnt[mid] = c - x;
+}
+
+// Per row: never-jumpers and their score, jumper count.  Fixed grid and
+// fixed in-block tree, so the partial tallies are deterministic.
+__global__ void __launch_bounds__(kRowsThreads)
+vec_rows_kernel(const uint64_t* __restrict__ cnt, const double* __restrict__ rate,
+                const double* __restrict__ d, uint64_t n, FastParams p, double v_sum,
+                double* __restrict__ values, uint64_t* __restrict__ jcount,
+                double2* __restrict__ rowc, double* __restrict__ part_s1,
+                double* __restrict__ part_s2) {
+    __shared__ double sh1[kRowsThreads / 32], sh2[kRowsThreads / 32];
+    double s1 = 0.0, s2 = 0.0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t c = cnt[i];
+        uint64_t n0 = 0;
+        double tot = 0.0;
+        if (c) {
+            const double lam = __dmul_rn(rate[i], p.beta);
+            n0 = binomial(c, exp(-lam), (uint32_t)i, (uint32_t)(i >> 32), kTagStay, p.rk);
+            if (n0 < c)  // jumper constants: 1 - e^{-λ}, grid units per unit of R
+                rowc[i] = make_double2(-expm1(-lam), __ddiv_rn(p.inv_dt, rate[i]));
+            if (n0) {
+                // the never-jumper's weight, formed exactly as a walker that
+                // finishes at its start would form it (vec_walk_kernel)
+                const double di = d[i];
+                const double S = __dmul_rn(di, p.n_grid1);
+                const double corr = p.strang ? __dadd_rn(__dmul_rn(0.5, di), __dmul_rn(0.5, di))
+                                             : di;
+                const double f0 = __dmul_rn(v_sum, exp(__dmul_rn(p.dt, __dsub_rn(S, corr))));
+                tot = __dmul_rn((double)n0, f0);
+                s1 = __dadd_rn(s1, tot);
+                s2 = __fma_rn(tot, f0, s2);
+            }
+        }
+        if (values) values[i] = tot;
+        jcount[i] = c - n0;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s1 = __dadd_rn(s1, __shfl_xor_sync(0xffffffffu, s1, o));
+        s2 = __dadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, o));
+    }
+    if (lane == 0) { sh1[warp] = s1; sh2[warp] = s2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < kRowsThreads / 32; ++k) {
+            s1 = __dadd_rn(s1, sh1[k]);
+            s2 = __dadd_rn(s2, sh2[k]);
+        }
+        part_s1[blockIdx.x] = s1;
+        part_s2[blockIdx.x] = s2;
+    }
+}
+
+// row_of[q - q0] = the start row of jumper q, for q in [q0, q1).  Lane r of a
+// warp tests row (base + r); the warp then writes each overlapping row's
+// slice cooperatively (coalesced).
+__global__ void expand_rows_kernel(const uint64_t* __restrict__ off, uint64_t n, uint64_t q0,
+                                   uint64_t q1, uint32_t* __restrict__ row_of) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t base = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x - lane);
+         base < n; base += warps * 32) {
+        const uint64_t i = base + lane;
+        uint64_t a = 0, b = 0;
+        if (i < n) {
+            a = off[i];
+            b = off[i + 1];
+            a = a > q0 ? a : q0;
+            b = b < q1 ? b : q1;
+        }
+        unsigned hit = __ballot_sync(0xffffffffu, a < b);
+        while (hit) {
+            const int src = __ffs(hit) - 1;
+            hit &= hit - 1;
+            const uint64_t sa = __shfl_sync(0xffffffffu, a, src);
+            const uint64_t sb = __shfl_sync(0xffffffffu, b, src);
+            for (uint64_t q = sa + lane; q < sb; q += 32) row_of[q - q0] = (uint32_t)(base + src);
+        }
+    }
+}
+
+// Jumper walks q in [q0, q1), one lane per walker, static grid-stride
+// assignment (consecutive lanes: consecutive jumpers, mostly of one row).
+// Jumper k of row i draws its j-th jump from Philox (j, k_lo, i,
+// 'VECT' ^ k_hi) — y,w: 64-bit neighbour pick, z: alias coin — and x gives
+// the holding time at the state it lands on (j >= 1) or, for j = 0, the
+// truncated first holding time R at the start.  Lie weights sit on the state each
+// segment leaves from (estimator.cpp:228-231).
+__global__ void __launch_bounds__(128)
+vec_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj,
+                const uint32_t* __restrict__ thr, const uint32_t* __restrict__ alias,
+                const double2* __restrict__ rowc, const uint32_t* __restrict__ row_of,
+                const uint64_t* __restrict__ off_j, FastParams p, double v_sum, uint64_t q0,
+                uint64_t q1, uint32_t* __restrict__ out_end, double* __restrict__ out_f,
+                double* __restrict__ part_s1, double* __restrict__ part_s2,
+                unsigned long long* __restrict__ part_j) {
+    __shared__ double sh1[4], sh2[4];
+    __shared__ unsigned long long shj[4];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t q = q0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    double s1 = 0.0, s2 = 0.0;
+    unsigned long long jt = 0;
+    bool active = false;
+    uint32_t i = 0, cur = 0, off = 0, degf = 0, step = 0, jc = 0, klo = 0, tagv = 0;
+    float ir = 0.f;
+    double dcur = 0.0, t = 0.0, S = 0.0, g = 0.0, corr0 = 0.0;
+    while (true) {
+        if (!active) {
+            if (q >= q1) break;
+            i = __ldg(row_of + (q - q0));
+            const uint64_t k = q - __ldg(off_j + i);
+            klo = (uint32_t)k;
+            const uint32_t khi = (uint32_t)(k >> 32);
+            tagv = kTagScatter ^ khi;
+            const RowRec rs = load_rec(rec, i);
+            const double2 rc = __ldg(rowc + i);  // {1 - e^{-λ_i}, N / (β rate_i)}
+            const U4 w = philox4x32_10(U4{0u, klo, i, tagv}, p.rk);
+            // first holding time R / rate_i, R ~ Exp(1) truncated to [0, λ):
+            // R = -log1p(-u (1 - e^{-λ})), u from w.x; the jump from w.y, w.w, w.z
+            const float u = __fmul_rn(__uint2float_rn(w.x >> 8) + 0.5f, 0x1.0p-24f);
+            const float R = -log1pf(-__fmul_rn(u, (float)rc.x));
+            double tn = __dmul_rn((double)R, rc.y);
+            if (!(tn < p.n_grid)) tn = __dmul_rn(p.n_grid, 1.0 - 0x1.0p-53);
+            corr0 = p.strang ? __dmul_rn(0.5, rs.d) : 0.0;
+            // first sojourn at the start: credit its grid points, then jump
+            const double kk = ceil(tn);
+            S = __dmul_rn(rs.d, kk);
+            g = kk;
+            t = tn;
+            const Edge e = jump_edge(w.y, w.w, w.z, rs.off, rs.deg_flags, adj, thr, alias);
+            cur = e.j; off = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d;
+            jc = 1;
+            step = 1;
+            active = true;
+        }
+        const U4 w = philox4x32_10(U4{step, klo, i, tagv}, p.rk);
+        const float h = __fmul_rn(neg_ln_u(w.x), ir);
+        const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
+        if (tn >= p.n_grid) {
+            S = __fma_rn(dcur, __dsub_rn(p.n_grid1, g), S);
+            const double corr = p.strang ? __dadd_rn(corr0, __dmul_rn(0.5, dcur)) : dcur;
+            const double f = __dmul_rn(v_sum, exp(__dmul_rn(p.dt, __dsub_rn(S, corr))));
+            s1 = __dadd_rn(s1, f);
+            s2 = __fma_rn(f, f, s2);
+            jt += jc;
+            if (out_end) {
+                out_end[q - q0] = cur;
+                out_f[q - q0] = f;
+            }
+            active = false;
+            q += stride;
+        } else {
+            const double kk = ceil(tn);
+            S = __fma_rn(dcur, __dsub_rn(kk, g), S);
+            g = kk;
+            t = tn;
+            const Edge e = jump_edge(w.y, w.w, w.z, off, degf, adj, thr, alias);
+            cur = e.j; off = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d;
+            ++jc;
+            ++step;
+        }
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s1 = __dadd_rn(s1, __shfl_xor_sync(0xffffffffu, s1, o));
+        s2 = __dadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, o));
+        jt += __shfl_xor_sync(0xffffffffu, jt, o);
+    }
+    if (lane == 0) { sh1[warp] = s1; sh2[warp] = s2; shj[warp] = jt; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < 4; ++k) {
+            s1 = __dadd_rn(s1, sh1[k]);
+            s2 = __dadd_rn(s2, sh2[k]);
+            jt += shj[k];
+        }
+        part_s1[blockIdx.x] = s1;
+        part_s2[blockIdx.x] = s2;
+        part_j[blockIdx.x] = jt;
+    }
+}
+
+__global__ void binomial_debug_kernel(uint64_t n, double p, uint64_t count, PhiloxKeys K,
+                                      uint64_t* __restrict__ out) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        out[k] = binomial(n, p, (uint32_t)k, (uint32_t)(k >> 32), kTagDebug, K);
+}
+
+int tree_depth(uint64_t n) {
+    int D = 0;
+    while ((1ull << D) < n) ++D;
+    return D;
+}
+
+}  // namespace
+
+unsigned vec_rows_grid() { return kRowsBlocks; }
+unsigned vec_walk_grid() { return 148 * 12; }
+
+int launch_start_counts(uint64_t n, uint64_t M, const double* cum, const PhiloxKeys& K,
+                        uint64_t* cnt, cudaStream_t s) {
+    cudaMemsetAsync(cnt, 0, n * 8, s);
+    cudaMemcpyAsync(cnt, &M, 8, cudaMemcpyHostToDevice, s);  // pageable: staged synchronously
+    const int D = tree_depth(n);
+    for (int L = 0; L < D; ++L) {
+        const uint64_t nodes = 1ull << L;
+        tree_level_kernel<<<(unsigned)((nodes + 255) / 256), 256, 0, s>>>(cnt, n, D, L, cum, K);
+    }
+    return D;
+}
+
+void launch_vec_rows(const DevSplit& m, const uint64_t* cnt, const FastParams& p, double v_sum,
+                     double* values, uint64_t* jcount, double2* rowc, double* part_s1, double* part_s2,
+                     cudaStream_t s) {
+    vec_rows_kernel<<<kRowsBlocks, kRowsThreads, 0, s>>>(cnt, m.rate, m.d, m.n, p, v_sum, values,
+                                                          jcount, rowc, part_s1, part_s2);
+}
+
+size_t scan_u64_temp_bytes(uint64_t count) {
+    size_t b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (int64_t)count);
+    return b;
+}
+
+void launch_scan_u64(const uint64_t* in, uint64_t* out, uint64_t count, void* temp,
+                     size_t temp_bytes, cudaStream_t s) {
+    cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, (int64_t)count, s);
+}
+
+void launch_expand_rows(const uint64_t* off, uint64_t n, uint64_t q0, uint64_t q1,
+                        uint32_t* row_of, cudaStream_t s) {
+    const uint64_t warps = (n + 31) / 32;
+    const unsigned blocks = (unsigned)std::min<uint64_t>((warps + 7) / 8, 148 * 16);
+    expand_rows_kernel<<<blocks, 256, 0, s>>>(off, n, q0, q1, row_of);
+}
+
+void launch_vec_walk(const DevSplit& m, const double2* rowc, const uint32_t* row_of, const uint64_t* off,
+                     const FastParams& p, double v_sum, uint64_t q0, uint64_t q1,
+                     uint32_t* out_end, double* out_f, double* part_s1, double* part_s2,
+                     unsigned long long* part_j, cudaStream_t s) {
+    vec_walk_kernel<<<vec_walk_grid(), 128, 0, s>>>(m.rec, m.adj, m.alias_thr, m.alias_idx,
+                                                    rowc, row_of, off, p, v_sum, q0, q1,
+                                                    out_end, out_f, part_s1, part_s2, part_j);
+}
+
+void launch_binomial_debug(uint64_t n, double p, uint64_t count, const PhiloxKeys& K,
+                           uint64_t* out, cudaStream_t s) {
+    if (count == 0) return;
+    binomial_debug_kernel<<<148 * 4, 256, 0, s>>>(n, p, count, K, out);
+}
+
+}  // namespace expmc_b200

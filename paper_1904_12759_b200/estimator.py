@@ -342,5 +342,28 @@ def gather_ceiling_device(m: SplitMatrix, rows_ptr: int, nrows: int, chains_per_
                                                  stream or None))
 
 
+def binomial_samples(trials: int, p: float, count: int, seed: int = 0,
+                     device: int = 0) -> np.ndarray:
+    """`count` draws of K4's device Binomial(trials, p) sampler (test hook)."""
+    out = np.zeros(int(count), dtype=np.uint64)
+    check(lib().expmc_cuda_binomial_samples(int(device), int(trials), float(p), int(count),
+                                            int(seed), out.ctypes.data_as(u64p)))
+    return out
+
+
+def start_counts(m: SplitMatrix, v, samples: int, seed: int) -> np.ndarray:
+    """K4's walkers per start row ~ Multinomial(samples, v / V) (v None: uniform),
+    the draw vector_estimate / tc_estimate make for (samples, seed)."""
+    out = np.zeros(m.n, dtype=np.uint64)
+    if v is None:
+        vp_, nv = None, 0
+    else:
+        v = _f64(v)
+        vp_, nv = v.ctypes.data_as(f64p), len(v)
+    check(lib().expmc_cuda_start_counts(m.handle, vp_, nv, int(samples), int(seed),
+                                        out.ctypes.data_as(u64p)))
+    return out
+
+
 def launch_count() -> int:
     return int(lib().expmc_cuda_launch_count())

@@ -1,0 +1,205 @@
+"""K4 (vector_estimate / tc_estimate by grouped starts, csrc/walk_vec.cu) on the GPU.
+
+K4 draws the reference's M i.i.d. walkers (estimator.cpp:208-318) grouped by
+start row: multinomial start counts down a binomial tree, a binomial split of
+each row's walkers into never-jumpers and jumpers, walks for the jumpers only.
+These tests pin the two samplers that replace the per-walker start draw
+against their exact laws, then the estimators against the reference.
+
+Tolerances (written here, per the contract):
+  * Binomial sampler: chi-square goodness of fit against scipy.stats.binom,
+    p-value > 1e-4 per case (cells with expected count >= 20), and the sample
+    mean within 5 standard errors of n p.
+  * Start counts: sum exactly M; chi-square of the counts against M v / V
+    (one multinomial draw: n - 1 degrees of freedom), p-value > 1e-4.
+  * Estimates: global functional within 4 combined SE of the reference's own
+    vector_estimate / tc_estimate; per entry, against the splitting product x
+    the walkers sample (K5): the mean of R = 8 GPU runs within 1.5 / sqrt(R)
+    of a single run's L1 distance (no per-entry bias), and the reference's
+    L1 distance within a factor 1.6 of a GPU run's; total jumps within 1%.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+stats = pytest.importorskip("scipy.stats")
+
+
+def _chi2_binom(x, n, p):
+    dist = stats.binom(n, p)
+    lo, hi = int(x.min()), int(x.max())
+    ks = np.arange(lo, hi + 1)
+    pmf = dist.pmf(ks)
+    # merge tails into the edge cells, then merge cells until expected >= 20
+    pmf[0] += dist.cdf(lo - 1)
+    pmf[-1] += dist.sf(hi)
+    obs = np.bincount((x - lo).astype(np.int64), minlength=len(ks)).astype(float)
+    exp = pmf * len(x)
+    cells_o, cells_e, ao, ae = [], [], 0.0, 0.0
+    for o, e in zip(obs, exp):
+        ao += o
+        ae += e
+        if ae >= 20:
+            cells_o.append(ao)
+            cells_e.append(ae)
+            ao = ae = 0.0
+    if ae > 0 and cells_e:
+        cells_o[-1] += ao
+        cells_e[-1] += ae
+    cells_o, cells_e = np.array(cells_o), np.array(cells_e)
+    cells_e *= cells_o.sum() / cells_e.sum()
+    if len(cells_o) < 2:
+        return 1.0
+    return stats.chisquare(cells_o, cells_e).pvalue
+
+
+@pytest.mark.parametrize("n,p", [
+    (1, 0.3), (7, 0.5), (40, 0.1), (1000, 0.005),      # inversion (n p < 10)
+    (30, 0.4), (1000, 0.02), (10_000, 0.5),            # BTRS
+    (123_456_789, 1e-7), (2_000_000_000, 0.3),         # BTRS, large n
+    (500, 0.97), (10_000_000_000, 0.999999),           # p > 1/2 (symmetry)
+])
+def test_binomial_sampler_law(pb, n, p):
+    x = pb.binomial_samples(n, p, 400_000, seed=11).astype(np.float64)
+    assert x.min() >= 0 and x.max() <= n
+    mean, var = n * p, n * p * (1 - p)
+    assert abs(x.mean() - mean) <= 5 * math.sqrt(var / len(x)) + 1e-12
+    if var > 0:
+        assert abs(x.var() / var - 1) < 0.02
+    if var < 1e7:  # pmf cells resolvable
+        assert _chi2_binom(x, n, p) > 1e-4
+
+
+def test_binomial_sampler_edges(pb):
+    assert np.all(pb.binomial_samples(0, 0.5, 100) == 0)
+    assert np.all(pb.binomial_samples(50, 0.0, 100) == 0)
+    assert np.all(pb.binomial_samples(50, 1.0, 100) == 50)
+    a = pb.binomial_samples(1000, 0.3, 1000, seed=3)
+    b = pb.binomial_samples(1000, 0.3, 1000, seed=3)
+    c = pb.binomial_samples(1000, 0.3, 1000, seed=4)
+    assert np.array_equal(a, b) and not np.array_equal(a, c)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 37, 1000, 4097])
+def test_start_counts_multinomial(pb, n):
+    rng = np.random.default_rng(n)
+    csr = pb.gen_ws(max(n, 12), 2, 0.1, 3) if n >= 12 else pb.csr_from_dense(
+        np.ones((n, n)) - np.eye(n) if n > 1 else np.zeros((1, 1)))
+    m = pb.split(csr)
+    nn = m.n
+    M = 10_000_000
+    for v in (None, rng.uniform(0, 1, nn) * (rng.uniform(size=nn) > 0.2)):
+        if v is not None and v.sum() == 0:
+            v[0] = 1.0
+        c = pb.start_counts(m, v, M, seed=5)
+        assert c.sum() == M
+        w = np.ones(nn) if v is None else v
+        if v is not None:
+            assert np.all(c[w == 0] == 0)
+        e = M * w / w.sum()
+        keep = e > 0
+        if keep.sum() > 1:
+            assert stats.chisquare(c[keep], e[keep]).pvalue > 1e-4
+        c2 = pb.start_counts(m, v, M, seed=5)
+        assert np.array_equal(c, c2)
+
+
+def test_start_counts_many_seeds_mean(pb):
+    """Across seeds, each row's count averages M p_i (unbiased tree)."""
+    csr = pb.gen_ws(300, 2, 0.1, 1)
+    m = pb.split(csr)
+    v = np.linspace(0.1, 3.0, m.n)
+    M = 100_000
+    acc = np.zeros(m.n)
+    S = 200
+    for s in range(S):
+        acc += pb.start_counts(m, v, M, seed=100 + s)
+    p = v / v.sum()
+    z = (acc / S - M * p) / np.sqrt(M * p * (1 - p) / S)
+    assert abs(z.mean()) < 4 / math.sqrt(m.n) * 2 and 0.7 < z.var() < 1.3
+
+
+@pytest.mark.parametrize("splitting", [0, 1])
+@pytest.mark.parametrize("name", ["ba_2000", "weighted_40", "ws_3000"])
+def test_vector_and_tc_vs_reference(pb, ref, name, splitting):
+    from test_gpu_parity import _graphs
+
+    csr = _graphs(pb)[name]
+    rm = ref.matrix_from_csr(csr)
+    m = pb.split(csr)
+    rng = np.random.default_rng(7)
+    v = rng.uniform(0, 1, csr.n)
+    v[rng.uniform(size=csr.n) < 0.1] = 0.0
+    beta = {"ba_2000": 0.05, "weighted_40": 0.7, "ws_3000": 0.3}[name]
+    M = 4_000_000
+    p = pb.PathParams(beta, 32, M, pb.Splitting(splitting), 9)
+    got = pb.vector_estimate(m, v, p)
+    rv, rse, rj, rvs = rm.vector_estimate(v, beta, 32, M, splitting, 10, workers=16)
+    z = (got.values.sum() - rv.sum()) / math.sqrt(got.std_error_global ** 2 + rse ** 2)
+    assert abs(z) < 4.0, z
+    # per-entry law: E[values] is the splitting product x (K5, deterministic).
+    # R independent GPU runs: their mean must close in on x as 1/sqrt(R) (no
+    # per-entry bias), and the reference's distance to x must match a single
+    # GPU run's (same per-entry noise).
+    x = pb.splitting_product(m, v, p)
+    R = 8
+    runs = [got.values] + [pb.vector_estimate(
+        m, v, pb.PathParams(beta, 32, M, pb.Splitting(splitting), 1000 + r)).values
+        for r in range(R - 1)]
+    l1 = lambda y: np.abs(y - x).sum() / np.abs(x).sum()
+    e_single = np.mean([l1(y) for y in runs])
+    e_mean = l1(np.mean(runs, axis=0))
+    e_ref = l1(rv)
+    assert e_mean < 1.5 * e_single / math.sqrt(R), (e_mean, e_single)
+    assert e_single / 1.6 < e_ref < 1.6 * e_single, (e_ref, e_single)
+    assert abs(got.total_jumps / rj - 1) < 0.01
+    t = pb.tc_estimate(m, p)
+    tv, tse, tj = rm.tc_estimate(beta, 32, M, splitting, 10, workers=16)
+    assert abs(t.value - tv) < 4.0 * math.sqrt(t.std_error ** 2 + tse ** 2)
+
+
+def test_vector_matches_splitting_product(pb):
+    """K4 values against the deterministic splitting product (K5) the walkers
+    sample, on a graph with hubs: per-entry z over the rows that collect many
+    walkers, and the global functional."""
+    csr = pb.gen_ba(3000, 4, 2)
+    m = pb.split(csr)
+    v = pb.gen_vector(0, csr.n, 5) + 0.05
+    p = pb.PathParams(0.05, 32, 30_000_000, pb.Splitting.Strang, 3)
+    got = pb.vector_estimate(m, v, p)
+    x = pb.splitting_product(m, v, p)
+    assert abs(got.values.sum() - x.sum()) < 4 * got.std_error_global
+    rel = np.abs(got.values - x).sum() / np.abs(x).sum()
+    assert rel < 0.03, rel
+
+
+def test_isolated_rows_and_single_row(pb, ref):
+    """Rows with rate 0 never jump (exp_time returns +inf, sampler.cpp:12):
+    all their walkers score at their start."""
+    a = np.zeros((5, 5))
+    a[0, 1] = a[1, 0] = 2.0
+    np.fill_diagonal(a, [0.1, -0.2, 0.3, -0.4, 0.5])
+    csr = pb.csr_from_dense(a)
+    m = pb.split(csr)
+    v = np.array([1.0, 2.0, 3.0, 0.0, 5.0])
+    p = pb.PathParams(1.0, 16, 2_000_000, pb.Splitting.Strang, 4)
+    got = pb.vector_estimate(m, v, p)
+    V = v.sum()
+    for i in (2, 3, 4):  # isolated: value_i = v_i e^{β a_ii} exactly in law; counts ~ v_i / V
+        exp_i = v[i] * math.exp(a[i, i])
+        if v[i] == 0:
+            assert got.values[i] == 0
+        else:
+            sd = V * math.exp(a[i, i]) * math.sqrt(v[i] / V * (1 - v[i] / V) / p.samples)
+            assert abs(got.values[i] - exp_i) < 5 * sd
+    rm = ref.matrix_from_csr(csr)
+    rv, rse, rj, _ = rm.vector_estimate(v, 1.0, 16, 2_000_000, 1, 4, workers=16)
+    z = (got.values.sum() - rv.sum()) / math.sqrt(got.std_error_global ** 2 + rse ** 2)
+    assert abs(z) < 4
+    one = pb.split(pb.csr_from_dense(np.array([[0.25]])))
+    r = pb.vector_estimate(one, [2.0], pb.PathParams(2.0, 8, 1000, seed=1))
+    assert r.values[0] == pytest.approx(2.0 * math.exp(0.5), rel=1e-14)
+    assert r.std_error_global <= 1e-6 * r.values[0] and r.total_jumps == 0
