@@ -152,6 +152,10 @@ uint32_t expmc_cuda_entry_slots(uint64_t walkers);
 /* Number of kernels this library has launched in this process. */
 uint64_t expmc_cuda_launch_count(void);
 
+/* Jumpers (walkers with at least one jump, i.e. walks actually run) of the
+ * last vector / tc estimate on this handle (K4; 0 before the first call). */
+int expmc_cuda_last_jumpers(const expmc_matrix* m, uint64_t* jumpers);
+
 /* ------------------------------------------- K4 sampler diagnostics (tests) */
 /* `count` draws of the device Binomial(trials, p) sampler used by the
  * Theorem-2 walkers (inversion / BTRS), Philox-keyed by seed, into out[]. */

@@ -150,6 +150,7 @@ struct expmc_matrix {
     DevBuf vdev, rows, out_val, out_se, out_j, fa, vcum, values, pa, pb, pc, scal, tmp1, tmp2,
         tmp3, iota, part, fa2, sort_tmp, lens, cnt, jcnt, joff, row_of, scan_tmp, rowc;
     uint64_t iota_n = 0;
+    uint64_t last_jumpers = 0;  // K4: jumpers of the last vector / tc call
     // host copies kept for K5 norm bounds
     std::vector<double> h_rate, h_diag;
 
@@ -643,6 +644,7 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
     CK(cudaStreamSynchronize(s));
     double sum = res[0], sq = res[1];
     uint64_t jumps = 0;
+    h->last_jumpers = J;
     // batch buffers sized by M (>= J), not by the random J, so repeated calls
     // with the same M never regrow (and re-allocate) them
     const uint64_t B = std::min<uint64_t>(M, 1ull << 26);
@@ -1158,6 +1160,13 @@ int expmc_cuda_entries_device(expmc_matrix* h, const uint32_t* rows_dev, uint64_
                                         value_dev, std_error_dev, jumps_dev, scratch,
                                         pick_stream(h, stream));
         after_launch(k);
+    });
+}
+
+int expmc_cuda_last_jumpers(const expmc_matrix* h, uint64_t* jumpers) {
+    return guarded([&] {
+        if (!h || !jumpers) throw InvalidArg("null argument");
+        *jumpers = h->last_jumpers;
     });
 }
 

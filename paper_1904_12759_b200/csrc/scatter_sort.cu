@@ -22,26 +22,47 @@ namespace {
 
 constexpr uint32_t kChunk = 32;  // records per thread in the run-sum passes
 
+constexpr int kPieceThreads = 128;
+constexpr int kPad = kChunk + 1;  // smem row stride (bank-conflict-free chunk walks)
+constexpr size_t kPieceSmem = (size_t)kPieceThreads * kPad * (sizeof(uint32_t) + sizeof(double));
+
 // Pass A: thread k owns chunk [kC, kC + C) of the sorted records and sums
 // every run piece in it sequentially.  A run that starts and ends in the
 // chunk is added to values[] here; the piece of a run that started earlier
 // goes to head[k]; the piece of a run that starts here and continues past
-// the chunk goes to tail[k] (completed in pass B).
-__global__ void run_pieces_kernel(const uint32_t* __restrict__ keys, const double* __restrict__ f,
-                                  uint64_t count, double* __restrict__ head,
-                                  double* __restrict__ tail, double* __restrict__ values) {
-    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+// the chunk goes to tail[k] (completed in pass B).  The block's records are
+// staged through shared memory with coalesced loads first.
+__global__ void __launch_bounds__(kPieceThreads)
+run_pieces_kernel(const uint32_t* __restrict__ keys, const double* __restrict__ f,
+                  uint64_t count, double* __restrict__ head, double* __restrict__ tail,
+                  double* __restrict__ values) {
+    extern __shared__ double smem[];
+    double* sf = smem;
+    uint32_t* sk = reinterpret_cast<uint32_t*>(smem + kPieceThreads * kPad);
+    const uint64_t base = (uint64_t)blockIdx.x * kPieceThreads * kChunk;
+    for (uint32_t i = threadIdx.x; i < kPieceThreads * kChunk; i += kPieceThreads) {
+        if (base + i < count) {
+            const uint32_t slot = (i / kChunk) * kPad + i % kChunk;
+            sk[slot] = keys[base + i];
+            sf[slot] = f[base + i];
+        }
+    }
+    __syncthreads();
+    const uint64_t k = (uint64_t)blockIdx.x * kPieceThreads + threadIdx.x;
     const uint64_t lo = k * kChunk;
     if (lo >= count) return;
-    const uint64_t hi = lo + kChunk < count ? lo + kChunk : count;
-    uint64_t pos = lo;
-    while (pos < hi) {
-        const uint32_t key = keys[pos];
-        const bool started = pos > lo || lo == 0 || keys[lo - 1] != key;
-        double s = f[pos];
-        uint64_t j = pos + 1;
-        while (j < hi && keys[j] == key) s = __dadd_rn(s, f[j++]);
-        const bool ends = j < hi || hi == count || keys[hi] != key;
+    const uint32_t len = (uint32_t)(count - lo < kChunk ? count - lo : kChunk);
+    const uint32_t* ck = sk + threadIdx.x * kPad;
+    const double* cf = sf + threadIdx.x * kPad;
+    const bool last_chunk = lo + len == count;
+    uint32_t pos = 0;
+    while (pos < len) {
+        const uint32_t key = ck[pos];
+        const bool started = pos > 0 || lo == 0 || keys[lo - 1] != key;
+        double s = cf[pos];
+        uint32_t j = pos + 1;
+        while (j < len && ck[j] == key) s = __dadd_rn(s, cf[j++]);
+        const bool ends = j < len || last_chunk || keys[lo + len] != key;
         if (!started) head[k] = s;
         else if (ends) values[key] = __dadd_rn(values[key], s);
         else tail[k] = s;
@@ -103,9 +124,12 @@ void scatter_sort_accumulate(uint32_t* end, double* f, uint32_t* end_sorted, dou
     const size_t sort_bytes = (tb + 255) & ~(size_t)255;
     double* head = reinterpret_cast<double*>(static_cast<unsigned char*>(temp) + sort_bytes);
     double* tail = head + chunks;
-    const unsigned blocks = (unsigned)((chunks + 255) / 256);
-    run_pieces_kernel<<<blocks, 256, 0, s>>>(end_sorted, f_sorted, count, head, tail, values);
-    run_spans_kernel<<<blocks, 256, 0, s>>>(end_sorted, count, head, tail, values);
+    cudaFuncSetAttribute(run_pieces_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kPieceSmem);  // per device; cheap
+    run_pieces_kernel<<<(unsigned)((chunks + kPieceThreads - 1) / kPieceThreads), kPieceThreads,
+                        kPieceSmem, s>>>(end_sorted, f_sorted, count, head, tail, values);
+    run_spans_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, s>>>(end_sorted, count, head,
+                                                                      tail, values);
 }
 
 }  // namespace expmc_b200

@@ -342,6 +342,13 @@ def gather_ceiling_device(m: SplitMatrix, rows_ptr: int, nrows: int, chains_per_
                                                  stream or None))
 
 
+def last_jumpers(m: SplitMatrix) -> int:
+    """Walks K4 actually ran (walkers with >= 1 jump) in the last vector / tc call."""
+    out = C.c_uint64()
+    check(lib().expmc_cuda_last_jumpers(m.handle, C.byref(out)))
+    return int(out.value)
+
+
 def binomial_samples(trials: int, p: float, count: int, seed: int = 0,
                      device: int = 0) -> np.ndarray:
     """`count` draws of K4's device Binomial(trials, p) sampler (test hook)."""

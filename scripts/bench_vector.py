@@ -26,6 +26,18 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def _hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        for k in ("hbm_gbs", "hbm_GBps", "copy_gbs"):
+            if k in d:
+                return float(d[k])
+    except (OSError, ValueError):
+        pass
+    return 7700.0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", type=int, nargs="+", default=[1, 2, 3, 4])
@@ -89,6 +101,17 @@ def main():
                                                    f"{secs_c:.1f} s"}
                 line["speedup_transitions"] = line["gpu"]["transitions_per_s"] / \
                     line["cpu_reference"]["transitions_per_s"]
+            # roofline of the whole call (SURVEY §8d bytes, K4 form): 64 B per
+            # jump + 48 B per jumper (start record + 16-B result record)
+            jumpers = pb.last_jumpers(m)
+            b_alg = 64.0 * jumps / args.steps + 48.0 * jumpers
+            peak = _hbm_peak()
+            ach = b_alg / (secs / args.steps) / 1e9
+            line["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                                "frac": ach / peak, "traffic": None,
+                                "algorithmic_bytes_per_call": b_alg,
+                                "jumpers_per_call": jumpers,
+                                "scope": "whole host call (wall clock)"}
             print(json.dumps(line), flush=True)
 
 
