@@ -664,7 +664,7 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
     for (uint64_t q0 = 0; q0 < J; q0 += B) {
         const uint64_t q1 = std::min(J, q0 + B);
         launch_expand_rows(off, n, q0, q1, row_of, s);
-        launch_vec_walk(h->m, rowc, row_of, off, fp, v_sum, q0, q1, rec_end, rec_f, pa, pb, pc, s);
+        launch_vec_walk(h->m, rowc, row_of, fp, v_sum, q0, q1, rec_end, rec_f, pa, pb, pc, s);
         launch_final_reduce(pa, pb, pc, wparts, tot, tot + 1,
                             reinterpret_cast<unsigned long long*>(tot + 2), s);
         after_launch(3);

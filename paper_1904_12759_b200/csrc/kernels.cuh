@@ -127,7 +127,7 @@ void launch_scan_u64(const uint64_t* in, uint64_t* out, uint64_t count, void* te
                      size_t temp_bytes, cudaStream_t s);
 void launch_expand_rows(const uint64_t* off, uint64_t n, uint64_t q0, uint64_t q1,
                         uint32_t* row_of, cudaStream_t s);
-void launch_vec_walk(const DevSplit& m, const double2* rowc, const uint32_t* row_of, const uint64_t* off,
+void launch_vec_walk(const DevSplit& m, const double2* rowc, const uint32_t* row_of,
                      const FastParams& p, double v_sum, uint64_t q0, uint64_t q1,
                      uint32_t* out_end, double* out_f, double* part_s1, double* part_s2,
                      unsigned long long* part_j, cudaStream_t s);

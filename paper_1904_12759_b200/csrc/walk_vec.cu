@@ -19,15 +19,15 @@
 //      a walker stays put iff its first holding time exceeds β) score the
 //      deterministic f0 = V e^{β d_i} at their own row — added to values[i]
 //      directly, no scatter;
-//   3. the c_i - n0 jumpers, numbered k = 0, 1, ... inside their row, start
+//   3. the c_i - n0 jumpers, numbered q = 0, 1, ... in start-row order, start
 //      with a first holding time R / rate_i, R ~ Exp(1) truncated to [0, λ_i)
 //      (memorylessness), and continue as the continuous-clock walkers of K3;
 //      consecutive lanes walk jumpers of the same row, so the first gathers
 //      share L1 lines.  Their (end, f) records go through the deterministic
 //      sort-based per-end reduction (scatter_sort.cu).
 //
-// Every draw is keyed by position (tree node, row, jumper index within its
-// row), never by thread, and every floating-point sum has a fixed order, so
+// Every draw is keyed by position (tree node, row, global jumper index),
+// never by thread, and every floating-point sum has a fixed order, so
 // results are bitwise reproducible.
 #include <cub/device/device_scan.cuh>
 
@@ -228,8 +228,9 @@ __global__ void expand_rows_kernel(const uint64_t* __restrict__ off, uint64_t n,
 
 // Jumper walks q in [q0, q1), one lane per walker, static grid-stride
 // assignment (consecutive lanes: consecutive jumpers, mostly of one row).
-// Jumper k of row i draws its j-th jump from Philox (j, k_lo, i,
-// 'VECT' ^ k_hi) — y,w: 64-bit neighbour pick, z: alias coin — and x gives
+// Jumper q (global index: jumpers numbered in start-row order, a pure
+// function of the seed) draws its j-th jump from Philox (j, q_lo, 0,
+// 'VECT' ^ q_hi) — y,w: 64-bit neighbour pick, z: alias coin — and x gives
 // the holding time at the state it lands on (j >= 1) or, for j = 0, the
 // truncated first holding time R at the start.  Lie weights sit on the state each
 // segment leaves from (estimator.cpp:228-231).
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(128)
 vec_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj,
                 const uint32_t* __restrict__ thr, const uint32_t* __restrict__ alias,
                 const double2* __restrict__ rowc, const uint32_t* __restrict__ row_of,
-                const uint64_t* __restrict__ off_j, FastParams p, double v_sum, uint64_t q0,
+                FastParams p, double v_sum, uint64_t q0,
                 uint64_t q1, uint32_t* __restrict__ out_end, double* __restrict__ out_f,
                 double* __restrict__ part_s1, double* __restrict__ part_s2,
                 unsigned long long* __restrict__ part_j) {
@@ -251,17 +252,18 @@ vec_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj,
     uint32_t i = 0, cur = 0, off = 0, degf = 0, step = 0, jc = 0, klo = 0, tagv = 0;
     float ir = 0.f;
     double dcur = 0.0, t = 0.0, S = 0.0, g = 0.0, corr0 = 0.0;
+    // start row of the lane's next jumper, loaded one walker ahead
+    uint32_t inext = q < q1 ? __ldg(row_of + (q - q0)) : 0u;
     while (true) {
         if (!active) {
             if (q >= q1) break;
-            i = __ldg(row_of + (q - q0));
-            const uint64_t k = q - __ldg(off_j + i);
-            klo = (uint32_t)k;
-            const uint32_t khi = (uint32_t)(k >> 32);
-            tagv = kTagScatter ^ khi;
+            i = inext;
+            if (q + stride < q1) inext = __ldg(row_of + (q + stride - q0));
+            klo = (uint32_t)q;
+            tagv = kTagScatter ^ (uint32_t)(q >> 32);
             const RowRec rs = load_rec(rec, i);
             const double2 rc = __ldg(rowc + i);  // {1 - e^{-λ_i}, N / (β rate_i)}
-            const U4 w = philox4x32_10(U4{0u, klo, i, tagv}, p.rk);
+            const U4 w = philox4x32_10(U4{0u, klo, 0u, tagv}, p.rk);
             // first holding time R / rate_i, R ~ Exp(1) truncated to [0, λ):
             // R = -log1p(-u (1 - e^{-λ})), u from w.x; the jump from w.y, w.w, w.z
             const float u = __fmul_rn(__uint2float_rn(w.x >> 8) + 0.5f, 0x1.0p-24f);
@@ -280,7 +282,7 @@ vec_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj,
             step = 1;
             active = true;
         }
-        const U4 w = philox4x32_10(U4{step, klo, i, tagv}, p.rk);
+        const U4 w = philox4x32_10(U4{step, klo, 0u, tagv}, p.rk);
         const float h = __fmul_rn(neg_ln_u(w.x), ir);
         const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
         if (tn >= p.n_grid) {
@@ -384,12 +386,12 @@ void launch_expand_rows(const uint64_t* off, uint64_t n, uint64_t q0, uint64_t q
     expand_rows_kernel<<<blocks, 256, 0, s>>>(off, n, q0, q1, row_of);
 }
 
-void launch_vec_walk(const DevSplit& m, const double2* rowc, const uint32_t* row_of, const uint64_t* off,
+void launch_vec_walk(const DevSplit& m, const double2* rowc, const uint32_t* row_of,
                      const FastParams& p, double v_sum, uint64_t q0, uint64_t q1,
                      uint32_t* out_end, double* out_f, double* part_s1, double* part_s2,
                      unsigned long long* part_j, cudaStream_t s) {
     vec_walk_kernel<<<vec_walk_grid(), 128, 0, s>>>(m.rec, m.adj, m.alias_thr, m.alias_idx,
-                                                    rowc, row_of, off, p, v_sum, q0, q1,
+                                                    rowc, row_of, p, v_sum, q0, q1,
                                                     out_end, out_f, part_s1, part_s2, part_j);
 }
 
