@@ -128,6 +128,21 @@ int expmc_cuda_vector_estimate(expmc_matrix* m, const double* v, uint64_t nv,
                                double* v_sum);
 /* tc_estimate (estimator.cpp:280-318). */
 int expmc_cuda_tc_estimate(expmc_matrix* m, const expmc_path_params* p, expmc_estimate* out);
+/* One shard of vector_estimate / tc_estimate (multi-GPU): only
+ * the walkers whose start lies in rows [row_lo, row_hi) — the same walkers,
+ * with the same randomness, that the unsharded call runs there (Philox
+ * engine only).  values (n entries, may be NULL for the scalar functional) is
+ * this shard's per-end contribution divided by M; sum / sum_sq / total_jumps
+ * are its raw tallies.  Over a partition of the rows the shard values add up
+ * to vector_estimate's values and the tallies give its std_error_global via
+ * finalize (estimator.cpp:76-89); only the fp summation order differs. */
+int expmc_cuda_vector_estimate_rows(expmc_matrix* m, const double* v, uint64_t nv,
+                                    const expmc_path_params* p, uint64_t row_lo,
+                                    uint64_t row_hi, double* values, double* sum,
+                                    double* sum_sq, uint64_t* total_jumps);
+int expmc_cuda_tc_estimate_rows(expmc_matrix* m, const expmc_path_params* p, uint64_t row_lo,
+                                uint64_t row_hi, double* sum, double* sum_sq,
+                                uint64_t* total_jumps);
 
 /* -------------------------------------------- device-resident variants */
 /* Stage v (device pointer, n doubles) for subsequent *_device calls:

@@ -57,6 +57,11 @@ SIGNATURES = [
     ("expmc_cuda_vector_estimate", C.c_int,
      [vp, f64p, C.c_uint64, C.POINTER(PathParamsC), f64p, f64p, u64p, f64p]),
     ("expmc_cuda_tc_estimate", C.c_int, [vp, C.POINTER(PathParamsC), C.POINTER(EstimateC)]),
+    ("expmc_cuda_vector_estimate_rows", C.c_int,
+     [vp, f64p, C.c_uint64, C.POINTER(PathParamsC), C.c_uint64, C.c_uint64, f64p, f64p, f64p,
+      u64p]),
+    ("expmc_cuda_tc_estimate_rows", C.c_int,
+     [vp, C.POINTER(PathParamsC), C.c_uint64, C.c_uint64, f64p, f64p, u64p]),
     ("expmc_cuda_set_v_device", C.c_int, [vp, vp, C.c_uint64, vp]),
     ("expmc_cuda_entries_device", C.c_int,
      [vp, vp, C.c_uint64, C.POINTER(PathParamsC), vp, vp, vp, vp]),

@@ -610,9 +610,13 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
 // jumper counts -> exclusive scan -> jumper walks in batches, whose (end, f)
 // records go through the deterministic sort-based per-end reduction.
 // Tallies: row partials, then batch partials, added on the host in order.
+// Rows [lo, hi) only (a shard): the counts and the global jumper numbering
+// are computed for every row — identical on every shard — but only walkers
+// starting in [lo, hi) are scored and walked, so the shards of a partition
+// run exactly the walkers of the unsharded call.
 void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_path_params* p,
                  double* vals, double* values_host, double* sum_out, double* sq_out,
-                 uint64_t* jumps_out) {
+                 uint64_t* jumps_out, uint64_t lo = 0, uint64_t hi = ~0ull) {
     cudaStream_t s = h->stream;
     const uint64_t n = h->m.n, M = p->samples;
     const FastParams fp = fast_params(p, M);
@@ -628,7 +632,8 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
     unsigned long long* pc = h->pc.get<unsigned long long>(parts);
     double* tot = h->scal.get<double>(4);
     double2* rowc = h->rowc.get<double2>(n);
-    launch_vec_rows(h->m, cnt, fp, v_sum, vals, jc, rowc, pa, pb, s);
+    if (hi > n) hi = n;
+    launch_vec_rows(h->m, cnt, fp, v_sum, lo, hi, vals, jc, rowc, pa, pb, s);
     CK(cudaMemsetAsync(jc + n, 0, 8, s));
     CK(cudaMemsetAsync(pc, 0, rparts * sizeof(unsigned long long), s));
     launch_final_reduce(pa, pb, pc, rparts, tot, tot + 1,
@@ -638,10 +643,13 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
     launch_scan_u64(jc, off, n + 1, scan_tmp, scan_bytes, s);
     after_launch(3);
     double res[3];
-    uint64_t J = 0;
+    uint64_t qa = 0, qb = 0;  // the shard's jumpers
     CK(cudaMemcpyAsync(res, tot, sizeof(res), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&J, off + n, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&qa, off + std::min(lo, n), 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&qb, off + hi, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (qb < qa) qb = qa;
+    const uint64_t J = qb - qa;
     double sum = res[0], sq = res[1];
     uint64_t jumps = 0;
     h->last_jumpers = J;
@@ -661,8 +669,8 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
         temp_bytes = scatter_sort_temp_bytes(B, n);
         temp = h->sort_tmp.get<unsigned char>(temp_bytes);
     }
-    for (uint64_t q0 = 0; q0 < J; q0 += B) {
-        const uint64_t q1 = std::min(J, q0 + B);
+    for (uint64_t q0 = qa; q0 < qb; q0 += B) {
+        const uint64_t q1 = std::min(qb, q0 + B);
         launch_expand_rows(off, n, q0, q1, row_of, s);
         launch_vec_walk(h->m, rowc, row_of, fp, v_sum, q0, q1, rec_end, rec_f, pa, pb, pc, s);
         launch_final_reduce(pa, pb, pc, wparts, tot, tot + 1,
@@ -697,7 +705,7 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
 // Theorem 2 walkers (vector / tc).  start_mode 0 uniform, 1 categorical.
 void run_scatter(expmc_matrix* h, int start_mode, const std::vector<double>* cum, double v_sum,
                  const expmc_path_params* p, double* values_host, double* sum_out,
-                 double* sq_out, uint64_t* jumps_out) {
+                 double* sq_out, uint64_t* jumps_out, uint64_t lo = 0, uint64_t hi = ~0ull) {
     DeviceGuard g(h->device);
     cudaStream_t s = h->stream;
     const uint64_t n = h->m.n;
@@ -713,7 +721,7 @@ void run_scatter(expmc_matrix* h, int start_mode, const std::vector<double>* cum
         vc = c;
     }
     if (p->rng == EXPMC_RNG_PHILOX) {
-        run_grouped(h, vc, v_sum, p, vals, values_host, sum_out, sq_out, jumps_out);
+        run_grouped(h, vc, v_sum, p, vals, values_host, sum_out, sq_out, jumps_out, lo, hi);
         return;
     }
     const unsigned parts = scatter_compat_grid();
@@ -850,6 +858,38 @@ void expmv_dev(expmc_matrix* h, int mode, double t, double tol, double* x, cudaS
     after_launch(1);
 }
 
+}  // namespace
+
+namespace {
+// vector_estimate's checks and StartSampler table (estimator.cpp:208-222,
+// :92-128): returns V; cum stays empty for the exact-uniform case.
+double vector_setup(expmc_matrix* h, const double* v, uint64_t nv, const expmc_path_params* p,
+                    std::vector<double>& cum) {
+    if (!h) throw InvalidArg("matrix handle is null");
+    validate_params(p);
+    check_vector(h, v, nv);
+    double v_sum = 0.0;  // estimator.cpp:212-222
+    for (uint64_t k = 0; k < nv; ++k) {
+        if (v[k] < 0.0) throw InvalidArg("vector_estimate requires v >= 0 entrywise");
+        v_sum += v[k];
+    }
+    if (!(v_sum > 0.0)) throw InvalidArg("vector_estimate requires sum(v) > 0");
+    bool uniform = true;  // exact uniform test (estimator.cpp:95-100)
+    for (uint64_t k = 0; k < nv; ++k)
+        if (v[k] != v[0]) { uniform = false; break; }
+    cum.clear();
+    if (!uniform) {
+        cum.resize(nv);
+        double acc = 0.0;
+        for (uint64_t k = 0; k < nv; ++k) { acc += v[k]; cum[k] = acc; }
+    }
+    return v_sum;
+}
+
+void check_shard(const expmc_matrix* h, const expmc_path_params* p, uint64_t lo, uint64_t hi) {
+    if (lo > hi || hi > h->m.n) throw InvalidArg("row range out of bounds");
+    if (p->rng != EXPMC_RNG_PHILOX) throw InvalidArg("row shards need the Philox engine");
+}
 }  // namespace
 
 extern "C" {
@@ -1079,32 +1119,41 @@ int expmc_cuda_vector_estimate(expmc_matrix* h, const double* v, uint64_t nv,
                                double* std_error_global, uint64_t* total_jumps,
                                double* v_sum_out) {
     return guarded([&] {
-        if (!h) throw InvalidArg("matrix handle is null");
-        validate_params(p);
-        check_vector(h, v, nv);
-        double v_sum = 0.0;  // estimator.cpp:212-222
-        for (uint64_t k = 0; k < nv; ++k) {
-            if (v[k] < 0.0) throw InvalidArg("vector_estimate requires v >= 0 entrywise");
-            v_sum += v[k];
-        }
-        if (!(v_sum > 0.0)) throw InvalidArg("vector_estimate requires sum(v) > 0");
-        // StartSampler (estimator.cpp:92-128): exact uniform test, else cum
-        bool uniform = true;
-        for (uint64_t k = 0; k < nv; ++k)
-            if (v[k] != v[0]) { uniform = false; break; }
         std::vector<double> cum;
-        if (!uniform) {
-            cum.resize(nv);
-            double acc = 0.0;
-            for (uint64_t k = 0; k < nv; ++k) { acc += v[k]; cum[k] = acc; }
-        }
+        const double v_sum = vector_setup(h, v, nv, p, cum);
         double sum, sq;
         uint64_t j;
-        run_scatter(h, uniform ? 0 : 1, &cum, v_sum, p, values, &sum, &sq, &j);
+        run_scatter(h, cum.empty() ? 0 : 1, &cum, v_sum, p, values, &sum, &sq, &j);
         double value;
         finalize(sum, sq, p->samples, &value, std_error_global);
         *total_jumps = j;
         *v_sum_out = v_sum;
+    });
+}
+
+int expmc_cuda_vector_estimate_rows(expmc_matrix* h, const double* v, uint64_t nv,
+                                    const expmc_path_params* p, uint64_t row_lo,
+                                    uint64_t row_hi, double* values, double* sum,
+                                    double* sum_sq, uint64_t* total_jumps) {
+    return guarded([&] {
+        std::vector<double> cum;
+        const double v_sum = vector_setup(h, v, nv, p, cum);
+        check_shard(h, p, row_lo, row_hi);
+        run_scatter(h, cum.empty() ? 0 : 1, &cum, v_sum, p, values, sum, sum_sq, total_jumps,
+                    row_lo, row_hi);
+    });
+}
+
+int expmc_cuda_tc_estimate_rows(expmc_matrix* h, const expmc_path_params* p, uint64_t row_lo,
+                                uint64_t row_hi, double* sum, double* sum_sq,
+                                uint64_t* total_jumps) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        validate_params(p);
+        if (h->m.n == 0) throw InvalidArg("empty matrix");  // estimator.cpp:283
+        check_shard(h, p, row_lo, row_hi);
+        run_scatter(h, 0, nullptr, (double)h->m.n, p, nullptr, sum, sum_sq, total_jumps, row_lo,
+                    row_hi);
     });
 }
 

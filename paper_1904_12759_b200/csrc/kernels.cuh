@@ -120,7 +120,7 @@ unsigned vec_walk_grid();
 int launch_start_counts(uint64_t n, uint64_t M, const double* cum, const PhiloxKeys& K,
                         uint64_t* cnt, cudaStream_t s);
 void launch_vec_rows(const DevSplit& m, const uint64_t* cnt, const FastParams& p, double v_sum,
-                     double* values, uint64_t* jcount, double2* rowc, double* part_s1,
+                     uint64_t lo, uint64_t hi, double* values, uint64_t* jcount, double2* rowc, double* part_s1,
                      double* part_s2, cudaStream_t s);
 size_t scan_u64_temp_bytes(uint64_t count);
 void launch_scan_u64(const uint64_t* in, uint64_t* out, uint64_t count, void* temp,

@@ -145,11 +145,13 @@ __global__ void tree_level_kernel(uint64_t* __restrict__ cnt, uint64_t n, int D,
 }
 
 // Per row: never-jumpers and their score, jumper count.  Fixed grid and
-// fixed in-block tree, so the partial tallies are deterministic.
+// fixed in-block tree, so the partial tallies are deterministic.  Every row
+// gets its jumper count (the global jumper numbering), only rows in
+// [lo, hi) (the shard) score their never-jumpers.
 __global__ void __launch_bounds__(kRowsThreads)
 vec_rows_kernel(const uint64_t* __restrict__ cnt, const double* __restrict__ rate,
                 const double* __restrict__ d, uint64_t n, FastParams p, double v_sum,
-                double* __restrict__ values, uint64_t* __restrict__ jcount,
+                uint64_t lo, uint64_t hi, double* __restrict__ values, uint64_t* __restrict__ jcount,
                 double2* __restrict__ rowc, double* __restrict__ part_s1,
                 double* __restrict__ part_s2) {
     __shared__ double sh1[kRowsThreads / 32], sh2[kRowsThreads / 32];
@@ -164,7 +166,7 @@ vec_rows_kernel(const uint64_t* __restrict__ cnt, const double* __restrict__ rat
             n0 = binomial(c, exp(-lam), (uint32_t)i, (uint32_t)(i >> 32), kTagStay, p.rk);
             if (n0 < c)  // jumper constants: 1 - e^{-λ}, grid units per unit of R
                 rowc[i] = make_double2(-expm1(-lam), __ddiv_rn(p.inv_dt, rate[i]));
-            if (n0) {
+            if (n0 && i >= lo && i < hi) {
                 // the never-jumper's weight, formed exactly as a walker that
                 // finishes at its start would form it (vec_walk_kernel)
                 const double di = d[i];
@@ -361,9 +363,9 @@ int launch_start_counts(uint64_t n, uint64_t M, const double* cum, const PhiloxK
 }
 
 void launch_vec_rows(const DevSplit& m, const uint64_t* cnt, const FastParams& p, double v_sum,
-                     double* values, uint64_t* jcount, double2* rowc, double* part_s1, double* part_s2,
+                     uint64_t lo, uint64_t hi, double* values, uint64_t* jcount, double2* rowc, double* part_s1, double* part_s2,
                      cudaStream_t s) {
-    vec_rows_kernel<<<kRowsBlocks, kRowsThreads, 0, s>>>(cnt, m.rate, m.d, m.n, p, v_sum, values,
+    vec_rows_kernel<<<kRowsBlocks, kRowsThreads, 0, s>>>(cnt, m.rate, m.d, m.n, p, v_sum, lo, hi, values,
                                                           jcount, rowc, part_s1, part_s2);
 }
 

@@ -294,6 +294,40 @@ def vector_estimate(m: SplitMatrix, v, p: PathParams, workers: int = 1) -> Vecto
     return VectorEstimate(vals, se.value, p.samples, jm.value, vs.value)
 
 
+def vector_estimate_rows(m: SplitMatrix, v, p: PathParams, row_lo: int, row_hi: int):
+    """One row shard of vector_estimate (walkers starting in [row_lo, row_hi)):
+    (values / M contribution, Σf, Σf², jumps).  See shard.vector_estimate_sharded."""
+    v = _f64(v)
+    pc = p._c()
+    vals = np.zeros(m.n)
+    s1, s2, jm = C.c_double(), C.c_double(), C.c_uint64()
+    check(lib().expmc_cuda_vector_estimate_rows(m.handle, v.ctypes.data_as(f64p), len(v),
+                                                C.byref(pc), int(row_lo), int(row_hi),
+                                                vals.ctypes.data_as(f64p), C.byref(s1),
+                                                C.byref(s2), C.byref(jm)))
+    return vals, s1.value, s2.value, int(jm.value)
+
+
+def tc_estimate_rows(m: SplitMatrix, p: PathParams, row_lo: int, row_hi: int):
+    """One row shard of tc_estimate: (Σf, Σf², jumps) of its walkers."""
+    pc = p._c()
+    s1, s2, jm = C.c_double(), C.c_double(), C.c_uint64()
+    check(lib().expmc_cuda_tc_estimate_rows(m.handle, C.byref(pc), int(row_lo), int(row_hi),
+                                            C.byref(s1), C.byref(s2), C.byref(jm)))
+    return s1.value, s2.value, int(jm.value)
+
+
+def finalize(total: float, total_sq: float, samples: int, jumps: int) -> Estimate:
+    """estimator.cpp:76-89: mean, one-pass variance clamped at 0, SE."""
+    mm = float(samples)
+    value = total / mm
+    se = 0.0
+    if samples > 1:
+        var = max(0.0, (total_sq - total * total / mm) / (mm - 1.0))
+        se = math.sqrt(var / mm)
+    return Estimate(value, se, int(samples), int(jumps))
+
+
 def tc_estimate(m: SplitMatrix, p: PathParams, workers: int = 1) -> Estimate:
     """estimator.cpp:280-318 — total communicability (1, e^{βA} 1)."""
     pc = p._c()

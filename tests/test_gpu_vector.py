@@ -203,3 +203,38 @@ def test_isolated_rows_and_single_row(pb, ref):
     r = pb.vector_estimate(one, [2.0], pb.PathParams(2.0, 8, 1000, seed=1))
     assert r.values[0] == pytest.approx(2.0 * math.exp(0.5), rel=1e-14)
     assert r.std_error_global <= 1e-6 * r.values[0] and r.total_jumps == 0
+
+
+@pytest.mark.parametrize("shards", [2, 3, 7])
+def test_start_row_shards_reproduce_unsharded(pb, shards):
+    """Multi-GPU path of the Theorem-2 estimators, on one GPU:
+    the row shards run exactly the unsharded call's walkers, so their
+    rank-ordered combination equals vector_estimate / tc_estimate up to fp
+    summation order (1e-12), with identical jump counts."""
+    from paper_1904_12759_b200.shard import combine_tc_shards, combine_vector_shards, plan_shards
+
+    csr = pb.gen_ba(5000, 4, 3)
+    m = pb.split(csr)
+    v = pb.gen_vector(0, csr.n, 8) + 0.01
+    p = pb.PathParams(0.08, 32, 20_000_000, pb.Splitting.Strang, 21)
+    full = pb.vector_estimate(m, v, p)
+    parts = [pb.vector_estimate_rows(m, v, p, lo, hi) for lo, hi in plan_shards(csr.n, shards)]
+    got = combine_vector_shards(parts, p.samples, full.v_sum)
+    assert got.total_jumps == full.total_jumps
+    np.testing.assert_allclose(got.values, full.values, rtol=1e-12, atol=1e-14 * full.values.max())
+    assert got.std_error_global == pytest.approx(full.std_error_global, rel=1e-9)
+    t = pb.tc_estimate(m, p)
+    tp = combine_tc_shards([pb.tc_estimate_rows(m, p, lo, hi)
+                            for lo, hi in plan_shards(csr.n, shards)], p.samples)
+    assert tp.total_jumps == t.total_jumps
+    assert tp.value == pytest.approx(t.value, rel=1e-12)
+    assert tp.std_error == pytest.approx(t.std_error, rel=1e-9)
+
+
+def test_shard_argument_checks(pb):
+    m = pb.split(pb.gen_fd(2, 4, 1.0))
+    v = np.ones(m.n)
+    with pytest.raises(ValueError, match="row range out of bounds"):
+        pb.vector_estimate_rows(m, v, pb.PathParams(samples=10), 3, 2)
+    with pytest.raises(ValueError, match="row shards need the Philox engine"):
+        pb.tc_estimate_rows(m, pb.PathParams(samples=10, rng=pb.Rng.PCG_COMPAT), 0, 4)

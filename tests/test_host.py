@@ -193,6 +193,67 @@ def test_multi_rank_gather_gloo_is_bitwise_g_invariant(orc):
     assert np.array_equal(gj, j.astype(np.int64))
 
 
+def _fake_vector_shard(n, M):
+    """Deterministic stand-in for one rank's vector_estimate_rows (the CUDA
+    kernel cannot run here): depends only on the shard's row range."""
+    def fn(lo, hi):
+        r = np.random.default_rng(1000 + lo)
+        vals = r.uniform(size=n) / M
+        return vals, float(vals.sum() * M), float((vals ** 2).sum() * M * M), 2 ** 40 + 3 * lo + hi
+    return fn
+
+
+def _gloo_vec_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    sys.path.insert(0, ROOT)
+    from paper_1904_12759_b200.estimator import PathParams
+    from paper_1904_12759_b200.shard import tc_estimate_sharded, vector_estimate_sharded
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n, M = 97, 5000
+    v = np.linspace(0.5, 2.0, n)
+    p = PathParams(0.3, 16, M, seed=4)
+    fake = _fake_vector_shard(n, M)
+    ve = vector_estimate_sharded(None, v, p, shard_fn=fake)
+    te = tc_estimate_sharded(None, p, n, shard_fn=lambda lo, hi: fake(lo, hi)[1:])
+    if rank == 0:
+        q.put((ve.values.copy(), ve.std_error_global, ve.total_jumps, ve.v_sum, te))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_vector_and_tc_shards_combine_in_rank_order_gloo(world):
+    """Theorem-2 start-row shards over gloo ranks: per-end vectors and
+    tallies gathered and added in rank order, jumps (u64) carried exactly."""
+    import torch.multiprocessing as mp
+
+    from paper_1904_12759_b200.shard import combine_tc_shards, combine_vector_shards, plan_shards
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + world * 7 + os.getpid() % 500
+    procs = [ctx.Process(target=_gloo_vec_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    vals, se, jm, vs, te = q.get(timeout=120)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    n, M = 97, 5000
+    fake = _fake_vector_shard(n, M)
+    parts = [fake(lo, hi) for lo, hi in plan_shards(n, world)]
+    want = combine_vector_shards(parts, M, float(np.linspace(0.5, 2.0, n).sum()))
+    assert np.array_equal(vals, want.values) and se == want.std_error_global
+    assert jm == want.total_jumps == sum(p[3] for p in parts) and vs == want.v_sum
+    wt = combine_tc_shards([p[1:] for p in parts], M)
+    assert te == wt
+
+
 def test_bench_reference_arm_cpu(ref):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
                           "--config", "1", "--scale", "0.05", "--steps", "1", "--warmup", "0",
