@@ -380,6 +380,8 @@ def main():
         "data": "synthetic (seeded generators, SURVEY §8d)",
         "entries_per_s": total_entries / secs,
         "paths_per_s": total_entries * cfg.walkers / secs,
+        # segment-steps (N per path) for comparison with PAPER.md:314
+        "segment_steps_per_s": total_entries * cfg.walkers * cfg.n_steps / secs,
         "config": {"workload": f"cfg{cfg.idx}_{cfg.name}", "n": cfg.csr.n, "nnz": cfg.csr.nnz,
                    "entries": len(rows_all), "walkers_per_entry": cfg.walkers,
                    "n_steps": cfg.n_steps, "beta": cfg.beta, "splitting": "strang",

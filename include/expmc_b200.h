@@ -167,9 +167,11 @@ uint32_t expmc_cuda_entry_slots(uint64_t walkers);
 /* Number of kernels this library has launched in this process. */
 uint64_t expmc_cuda_launch_count(void);
 
-/* Jumpers (walkers with at least one jump, i.e. walks actually run) of the
- * last vector / tc estimate on this handle (K4; 0 before the first call). */
-int expmc_cuda_last_jumpers(const expmc_matrix* m, uint64_t* jumpers);
+/* K4 facts about the last vector / tc estimate on this handle: jumpers
+ * (walkers with at least one jump, i.e. walks actually run) and the per-end
+ * reduction used by vector_estimate (1: exact 128-bit fixed point, 0:
+ * sort-based, -1: none yet).  Either pointer may be NULL. */
+int expmc_cuda_last_k4_stats(const expmc_matrix* m, uint64_t* jumpers, int* fixed_point);
 
 /* ------------------------------------------- K4 sampler diagnostics (tests) */
 /* `count` draws of the device Binomial(trials, p) sampler used by the

@@ -6,7 +6,7 @@ The reference's estimator API (arXiv 1904.12759 C++ artifact,
 ``csrc/``.  There is no CPU fallback: every estimate runs on the GPU.
 """
 from ._lib import ExpmcError, lib
-from .estimator import (EntriesEstimate, binomial_samples, last_jumpers, start_counts, tc_estimate_rows,
+from .estimator import (EntriesEstimate, binomial_samples, last_jumpers, last_k4_stats, start_counts, tc_estimate_rows,
                         vector_estimate_rows, finalize, Estimate, PathParams, Rng, SplitMatrix, Splitting,
                         VectorEstimate, entries_device, entries_estimate, entry_estimate,
                         entry_slots, expmv, from_entries, from_matrix_market, gather_ceiling_device, launch_count, set_v_device,
@@ -17,7 +17,7 @@ from .inputs import (Csr, MmEntries, build_config, csr_from_dense, gen_ba, gen_f
 from .spectral import BetaRule, lambda_max, resolve_beta
 
 __all__ = [
-    "ExpmcError", "lib", "binomial_samples", "last_jumpers", "start_counts", "tc_estimate_rows",
+    "ExpmcError", "lib", "binomial_samples", "last_jumpers", "last_k4_stats", "start_counts", "tc_estimate_rows",
     "vector_estimate_rows", "finalize", "EntriesEstimate", "Estimate", "PathParams", "Rng", "SplitMatrix",
     "Splitting", "VectorEstimate", "entries_device", "entries_estimate", "entry_estimate",
     "entry_slots", "expmv", "gather_ceiling_device", "launch_count", "set_v_device", "split",

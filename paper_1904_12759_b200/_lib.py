@@ -68,7 +68,7 @@ SIGNATURES = [
     ("expmc_cuda_gather_ceiling_device", C.c_int,
      [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, vp]),
     ("expmc_cuda_entry_slots", C.c_uint32, [C.c_uint64]),
-    ("expmc_cuda_last_jumpers", C.c_int, [vp, u64p]),
+    ("expmc_cuda_last_k4_stats", C.c_int, [vp, u64p, C.POINTER(C.c_int)]),
     ("expmc_cuda_binomial_samples", C.c_int,
      [C.c_int, C.c_uint64, C.c_double, C.c_uint64, C.c_uint64, u64p]),
     ("expmc_cuda_start_counts", C.c_int, [vp, f64p, C.c_uint64, C.c_uint64, C.c_uint64, u64p]),

@@ -9,6 +9,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdio>
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -151,6 +152,10 @@ struct expmc_matrix {
         tmp3, iota, part, fa2, sort_tmp, lens, cnt, jcnt, joff, row_of, scan_tmp, rowc;
     uint64_t iota_n = 0;
     uint64_t last_jumpers = 0;  // K4: jumpers of the last vector / tc call
+    int last_fixed = -1;        // K4: 1 fixed-point per-end sums, 0 sort-based
+    double d_lo = 0.0, d_hi = 0.0;  // range of d (K4 fixed-point scale), once
+    bool d_range = false;
+    DevBuf acc;
     // host copies kept for K5 norm bounds
     std::vector<double> h_rate, h_diag;
 
@@ -165,7 +170,7 @@ struct expmc_matrix {
         for (void* p : owned) cudaFree(p);
         for (DevBuf* b : {&vdev, &rows, &out_val, &out_se, &out_j, &fa, &vcum, &values, &pa,
                           &pb, &pc, &scal, &tmp1, &tmp2, &tmp3, &iota, &part, &fa2, &sort_tmp, &lens, &cnt, &jcnt,
-                          &joff, &row_of, &scan_tmp, &rowc})
+                          &joff, &row_of, &scan_tmp, &rowc, &acc})
             b->release();
         if (stream) cudaStreamDestroy(stream);
         if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -661,7 +666,34 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
     double *rec_f = nullptr, *f_sorted = nullptr;
     void* temp = nullptr;
     size_t temp_bytes = 0;
+    // Per-end sums: exact 128-bit fixed point when every f = V w fits
+    // (w in [e^{β d_min}, e^{β d_max}]: M f_max 2^s < 2^127 and
+    // f_min 2^s >= 2^53), else the sort-based reduction.
+    unsigned long long* acc = nullptr;
+    int scale_exp = 0;
     if (vals) {
+        if (!h->d_range) {
+            std::vector<double> hd(n);
+            CK(cudaMemcpy(hd.data(), h->m.d, n * 8, cudaMemcpyDeviceToHost));
+            h->d_lo = n ? *std::min_element(hd.begin(), hd.end()) : 0.0;
+            h->d_hi = n ? *std::max_element(hd.begin(), hd.end()) : 0.0;
+            h->d_range = true;
+        }
+        const double lmax = std::log2(v_sum) + p->beta * h->d_hi / std::log(2.0) + 1.0;
+        const double lmin = std::log2(v_sum) + p->beta * h->d_lo / std::log(2.0) - 1.0;
+        const double lM = std::log2((double)M);
+        const int sx = (int)std::floor(126.0 - lM - lmax);
+        const bool fits = std::isfinite(lmax) && std::isfinite(lmin) && lmin + sx >= 54.0 &&
+                          sx - 64 > -1000 && sx - 64 < 1000 &&
+                          std::getenv("EXPMC_K4_SORT") == nullptr;  // A/B switch
+        if (fits) {
+            scale_exp = sx;
+            acc = h->acc.get<unsigned long long>(2 * n);
+            CK(cudaMemsetAsync(acc, 0, n * 16, s));
+        }
+        h->last_fixed = fits ? 1 : 0;
+    }
+    if (vals && !acc) {
         rec_end = h->tmp1.get<uint32_t>(B * 2);
         end_sorted = rec_end + B;
         rec_f = h->tmp2.get<double>(B * 2);
@@ -672,11 +704,12 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
     for (uint64_t q0 = qa; q0 < qb; q0 += B) {
         const uint64_t q1 = std::min(qb, q0 + B);
         launch_expand_rows(off, n, q0, q1, row_of, s);
-        launch_vec_walk(h->m, rowc, row_of, fp, v_sum, q0, q1, rec_end, rec_f, pa, pb, pc, s);
+        launch_vec_walk(h->m, rowc, row_of, fp, v_sum, q0, q1, rec_end, rec_f, acc,
+                        std::ldexp(1.0, scale_exp - 64), pa, pb, pc, s);
         launch_final_reduce(pa, pb, pc, wparts, tot, tot + 1,
                             reinterpret_cast<unsigned long long*>(tot + 2), s);
         after_launch(3);
-        if (vals) {
+        if (vals && !acc) {
             scatter_sort_accumulate(rec_end, rec_f, end_sorted, f_sorted, q1 - q0, n, temp,
                                     temp_bytes, vals, s);
             after_launch(3);
@@ -691,6 +724,10 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
         jumps += j;
     }
     CK(cudaGetLastError());
+    if (acc) {
+        launch_fixed_to_values(acc, n, std::ldexp(1.0, -scale_exp), vals, s);
+        after_launch(1);
+    }
     if (vals) {
         launch_scale(n, vals, 1.0 / (double)M, s);
         after_launch(1);
@@ -1212,10 +1249,11 @@ int expmc_cuda_entries_device(expmc_matrix* h, const uint32_t* rows_dev, uint64_
     });
 }
 
-int expmc_cuda_last_jumpers(const expmc_matrix* h, uint64_t* jumpers) {
+int expmc_cuda_last_k4_stats(const expmc_matrix* h, uint64_t* jumpers, int* fixed_point) {
     return guarded([&] {
-        if (!h || !jumpers) throw InvalidArg("null argument");
-        *jumpers = h->last_jumpers;
+        if (!h) throw InvalidArg("matrix handle is null");
+        if (jumpers) *jumpers = h->last_jumpers;
+        if (fixed_point) *fixed_point = h->last_fixed;
     });
 }
 

@@ -129,8 +129,11 @@ void launch_expand_rows(const uint64_t* off, uint64_t n, uint64_t q0, uint64_t q
                         uint32_t* row_of, cudaStream_t s);
 void launch_vec_walk(const DevSplit& m, const double2* rowc, const uint32_t* row_of,
                      const FastParams& p, double v_sum, uint64_t q0, uint64_t q1,
-                     uint32_t* out_end, double* out_f, double* part_s1, double* part_s2,
+                     uint32_t* out_end, double* out_f, unsigned long long* acc,
+                     double scale_hi, double* part_s1, double* part_s2,
                      unsigned long long* part_j, cudaStream_t s);
+void launch_fixed_to_values(const unsigned long long* acc, uint64_t n, double inv_scale,
+                            double* values, cudaStream_t s);
 void launch_binomial_debug(uint64_t n, double p, uint64_t count, const PhiloxKeys& K,
                            uint64_t* out, cudaStream_t s);
 

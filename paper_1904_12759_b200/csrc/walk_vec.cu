@@ -15,7 +15,7 @@
 //      differences of the reference's own cumulative table, so the leaf
 //      probabilities telescope to exactly the (cum[i] - cum[i-1]) / V the
 //      reference's upper_bound samples;
-//   2. per row, the never-jumpers n0 ~ Binomial(c_i, e^{-λ_i}) (λ_i = rate_i β:
+//   2. per row, the never-jumpers n0 = c_i - Binomial(c_i, 1 - e^{-λ_i}) (λ_i = rate_i β:
 //      a walker stays put iff its first holding time exceeds β) score the
 //      deterministic f0 = V e^{β d_i} at their own row — added to values[i]
 //      directly, no scatter;
@@ -163,9 +163,12 @@ vec_rows_kernel(const uint64_t* __restrict__ cnt, const double* __restrict__ rat
         double tot = 0.0;
         if (c) {
             const double lam = __dmul_rn(rate[i], p.beta);
-            n0 = binomial(c, exp(-lam), (uint32_t)i, (uint32_t)(i >> 32), kTagStay, p.rk);
+            // jumpers ~ Binomial(c, 1 - e^{-λ}), the jump probability from
+            // expm1 (no cancellation for small λ)
+            const double pj = -expm1(-lam);
+            n0 = c - binomial(c, pj, (uint32_t)i, (uint32_t)(i >> 32), kTagStay, p.rk);
             if (n0 < c)  // jumper constants: 1 - e^{-λ}, grid units per unit of R
-                rowc[i] = make_double2(-expm1(-lam), __ddiv_rn(p.inv_dt, rate[i]));
+                rowc[i] = make_double2(pj, __ddiv_rn(p.inv_dt, rate[i]));
             if (n0 && i >= lo && i < hi) {
                 // the never-jumper's weight, formed exactly as a walker that
                 // finishes at its start would form it (vec_walk_kernel)
@@ -197,6 +200,38 @@ vec_rows_kernel(const uint64_t* __restrict__ cnt, const double* __restrict__ rat
         }
         part_s1[blockIdx.x] = s1;
         part_s2[blockIdx.x] = s2;
+    }
+}
+
+// Order-independent exact per-end accumulation (vector_estimate, the
+// `local_values[out.end] += f` of estimator.cpp:250).  f >= 0 is added as
+// the 128-bit integer X = f 2^s (two 64-bit atomics with carry); integer
+// addition is exact and commutative, so the per-end totals do not depend on
+// the order in which walkers finish.  The host picks s so that M f_max 2^s <
+// 2^127 and f_min 2^s >= 2^53 (no bit of any f is lost); otherwise it uses
+// the sort-based reduction (scatter_sort.cu).
+__device__ __forceinline__ void fixed_add(unsigned long long* __restrict__ acc, uint32_t j,
+                                          double f, double scale_hi) {
+    const double y = __dmul_rn(f, scale_hi);  // f 2^s / 2^64 (power of 2: exact)
+    const double yh = floor(y);
+    const unsigned long long xh = (unsigned long long)yh;
+    const unsigned long long xl = (unsigned long long)__dmul_rn(__dsub_rn(y, yh), 0x1.0p64);
+    unsigned long long* a = acc + 2ull * j;
+    const unsigned long long old = atomicAdd(a, xl);
+    const unsigned long long hi = xh + (old + xl < old ? 1ull : 0ull);
+    if (hi) atomicAdd(a + 1, hi);
+}
+
+// values[j] += (hi 2^64 + lo) 2^-s
+__global__ void fixed_to_values_kernel(const unsigned long long* __restrict__ acc, uint64_t n,
+                                       double inv_scale, double* __restrict__ values) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long lo = acc[2 * j], hi = acc[2 * j + 1];
+        if (lo | hi) {
+            const double x = __fma_rn(__ull2double_rn(hi), 0x1.0p64, __ull2double_rn(lo));
+            values[j] = __dadd_rn(values[j], __dmul_rn(x, inv_scale));
+        }
     }
 }
 
@@ -242,6 +277,7 @@ vec_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj,
                 const double2* __restrict__ rowc, const uint32_t* __restrict__ row_of,
                 FastParams p, double v_sum, uint64_t q0,
                 uint64_t q1, uint32_t* __restrict__ out_end, double* __restrict__ out_f,
+                unsigned long long* __restrict__ acc, double scale_hi,
                 double* __restrict__ part_s1, double* __restrict__ part_s2,
                 unsigned long long* __restrict__ part_j) {
     __shared__ double sh1[4], sh2[4];
@@ -294,7 +330,9 @@ vec_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj,
             s1 = __dadd_rn(s1, f);
             s2 = __fma_rn(f, f, s2);
             jt += jc;
-            if (out_end) {
+            if (acc) {
+                fixed_add(acc, cur, f, scale_hi);
+            } else if (out_end) {
                 out_end[q - q0] = cur;
                 out_f[q - q0] = f;
             }
@@ -390,11 +428,18 @@ void launch_expand_rows(const uint64_t* off, uint64_t n, uint64_t q0, uint64_t q
 
 void launch_vec_walk(const DevSplit& m, const double2* rowc, const uint32_t* row_of,
                      const FastParams& p, double v_sum, uint64_t q0, uint64_t q1,
-                     uint32_t* out_end, double* out_f, double* part_s1, double* part_s2,
+                     uint32_t* out_end, double* out_f, unsigned long long* acc,
+                     double scale_hi, double* part_s1, double* part_s2,
                      unsigned long long* part_j, cudaStream_t s) {
     vec_walk_kernel<<<vec_walk_grid(), 128, 0, s>>>(m.rec, m.adj, m.alias_thr, m.alias_idx,
-                                                    rowc, row_of, p, v_sum, q0, q1,
-                                                    out_end, out_f, part_s1, part_s2, part_j);
+                                                    rowc, row_of, p, v_sum, q0, q1, out_end,
+                                                    out_f, acc, scale_hi, part_s1, part_s2,
+                                                    part_j);
+}
+
+void launch_fixed_to_values(const unsigned long long* acc, uint64_t n, double inv_scale,
+                            double* values, cudaStream_t s) {
+    fixed_to_values_kernel<<<148 * 8, 256, 0, s>>>(acc, n, inv_scale, values);
 }
 
 void launch_binomial_debug(uint64_t n, double p, uint64_t count, const PhiloxKeys& K,

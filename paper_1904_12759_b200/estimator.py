@@ -376,11 +376,18 @@ def gather_ceiling_device(m: SplitMatrix, rows_ptr: int, nrows: int, chains_per_
                                                  stream or None))
 
 
+def last_k4_stats(m: SplitMatrix):
+    """(jumpers, fixed_point) of the last vector / tc call on m: walks K4
+    actually ran, and whether vector_estimate's per-end sums used the exact
+    128-bit fixed point (1), the sort-based reduction (0) or none yet (-1)."""
+    j, fx = C.c_uint64(), C.c_int()
+    check(lib().expmc_cuda_last_k4_stats(m.handle, C.byref(j), C.byref(fx)))
+    return int(j.value), int(fx.value)
+
+
 def last_jumpers(m: SplitMatrix) -> int:
     """Walks K4 actually ran (walkers with >= 1 jump) in the last vector / tc call."""
-    out = C.c_uint64()
-    check(lib().expmc_cuda_last_jumpers(m.handle, C.byref(out)))
-    return int(out.value)
+    return last_k4_stats(m)[0]
 
 
 def binomial_samples(trials: int, p: float, count: int, seed: int = 0,

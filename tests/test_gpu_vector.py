@@ -238,3 +238,61 @@ def test_shard_argument_checks(pb):
         pb.vector_estimate_rows(m, v, pb.PathParams(samples=10), 3, 2)
     with pytest.raises(ValueError, match="row shards need the Philox engine"):
         pb.tc_estimate_rows(m, pb.PathParams(samples=10, rng=pb.Rng.PCG_COMPAT), 0, 4)
+
+
+def test_tiny_horizon_jump_counts(pb):
+    """λ = rate β ~ 1e-6: almost every walker stays put; the number of
+    jumpers (and jumps) must follow M E[1 - e^{-λ_start}] — the small-λ end
+    of the never-jumper split (jump probability from expm1, no cancellation)."""
+    csr = pb.gen_ws(2000, 5, 0.1, 9)
+    m = pb.split(csr)
+    beta = 1e-7
+    M = 200_000_000
+    rate = m.export()["rate"]
+    lam = rate * beta
+    expect = M * np.mean(-np.expm1(-lam))          # uniform starts (tc)
+    t = pb.tc_estimate(m, pb.PathParams(beta, 8, M, pb.Splitting.Strang, 5))
+    jumpers = pb.last_jumpers(m)
+    assert abs(jumpers - expect) < 5 * math.sqrt(expect), (jumpers, expect)
+    # second jumps within 1e-7 are ~λ times rarer: jumps ≈ jumpers
+    assert jumpers <= t.total_jumps < jumpers + 5 + 5 * math.sqrt(expect * lam.max() + 1)
+
+
+@pytest.mark.parametrize("name,beta", [("ba_2000", 0.05), ("weighted_40", 0.7),
+                                       ("fd3d_10", 0.004)])
+def test_fixed_point_and_sort_reductions_agree(pb, name, beta, monkeypatch):
+    """vector_estimate's two per-end reductions — exact 128-bit fixed point
+    (order-independent integer sums) and the sort-based sequential fp64 sums —
+    reduce the same walkers: per entry they agree to fp64 summation error,
+    and tallies / jumps are identical."""
+    from test_gpu_parity import _graphs
+
+    csr = _graphs(pb)[name]
+    m = pb.split(csr)
+    v = pb.gen_vector(0, csr.n, 4) + 0.02
+    p = pb.PathParams(beta, 32, 3_000_000, pb.Splitting.Lie, 17)
+    monkeypatch.delenv("EXPMC_K4_SORT", raising=False)
+    a = pb.vector_estimate(m, v, p)
+    assert pb.last_k4_stats(m)[1] == 1
+    monkeypatch.setenv("EXPMC_K4_SORT", "1")
+    b = pb.vector_estimate(m, v, p)
+    assert pb.last_k4_stats(m)[1] == 0
+    assert a.total_jumps == b.total_jumps and a.std_error_global == b.std_error_global
+    np.testing.assert_allclose(a.values, b.values, rtol=1e-12, atol=0)
+
+
+def test_fixed_point_falls_back_on_wide_weight_range(pb, ref):
+    """When e^{β (d_max - d_min)} times M does not fit the 128-bit window
+    (BA hubs at a large β), vector_estimate uses the sort-based reduction and
+    still agrees with the reference."""
+    csr = pb.gen_ba(2000, 5, 1)
+    m = pb.split(csr)
+    v = pb.gen_vector(0, csr.n, 4) + 0.02
+    beta = 0.6  # d_max ~ 150 -> e^{90}
+    p = pb.PathParams(beta, 64, 400_000, pb.Splitting.Strang, 2)
+    got = pb.vector_estimate(m, v, p)
+    assert pb.last_k4_stats(m)[1] == 0
+    rv, rse, _, _ = ref.matrix_from_csr(csr).vector_estimate(v, beta, 64, 400_000, 1, 3,
+                                                             workers=16)
+    z = (got.values.sum() - rv.sum()) / math.sqrt(got.std_error_global ** 2 + rse ** 2)
+    assert abs(z) < 4.0
