@@ -461,6 +461,76 @@ void upload_and_convert(uint64_t n, const uint32_t* rows, const uint32_t* cols, 
                         out);
 }
 
+// Entry estimator for samples >= 2^29 (walk_vec.cu, entry_big_*): rows and
+// outputs are device arrays on stream s; v must already be packed.
+void run_entries_big(expmc_matrix* h, const uint32_t* rows_d, uint64_t nrows,
+                     const expmc_path_params* p, double* value, double* se, uint64_t* jumps,
+                     cudaStream_t s) {
+    if (nrows == 0) return;
+    if (nrows >= (1ull << 32)) throw InvalidArg("at most 2^32 - 1 rows per call");
+    const uint64_t W = p->samples;
+    const FastParams fp = fast_params(p, W);
+    uint64_t* jc = h->jcnt.get<uint64_t>(nrows + 1);
+    uint64_t* off = h->joff.get<uint64_t>(nrows + 1);
+    double2* rowc = h->rowc.get<double2>(nrows);
+    double* Kr = h->fa.get<double>(nrows);
+    double* s1 = h->fa2.get<double>(2 * nrows);
+    double* s2 = s1 + nrows;
+    unsigned long long* jr = h->pc.get<unsigned long long>(std::max<uint64_t>(nrows, 1));
+    launch_entry_big_rows(h->m, rows_d, nrows, fp, jc, rowc, Kr, s1, s2, jr, s);
+    CK(cudaMemsetAsync(jc + nrows, 0, 8, s));
+    const size_t scan_bytes = scan_u64_temp_bytes(nrows + 1);
+    void* scan_tmp = h->scan_tmp.get<unsigned char>(scan_bytes);
+    launch_scan_u64(jc, off, nrows + 1, scan_tmp, scan_bytes, s);
+    after_launch(2);
+    // fixed-point windows: |dev| <= F = 2 e^{β d_max} max|v|, so W F 2^s1 <
+    // 2^125 (signed) and W F^2 2^s2 < 2^126
+    unsigned long long* vmax_d = h->scal.get<unsigned long long>(4) + 3;
+    CK(cudaMemsetAsync(vmax_d, 0, 8, s));
+    launch_rec_v_absmax(h->m, vmax_d, s);
+    after_launch(1);
+    uint64_t J = 0;
+    unsigned long long vbits = 0;
+    CK(cudaMemcpyAsync(&J, off + nrows, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&vbits, vmax_d, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double vmax;
+    std::memcpy(&vmax, &vbits, 8);
+    if (!h->d_range) {
+        std::vector<double> hd(h->m.n);
+        CK(cudaMemcpy(hd.data(), h->m.d, h->m.n * 8, cudaMemcpyDeviceToHost));
+        h->d_lo = *std::min_element(hd.begin(), hd.end());
+        h->d_hi = *std::max_element(hd.begin(), hd.end());
+        h->d_range = true;
+    }
+    const double lF = std::log2(vmax) + p->beta * h->d_hi / std::log(2.0) + 1.0;
+    // (the squares' window needs 2^(e2 - 64) to stay a normal double)
+    if (vmax > 0.0 && !(std::isfinite(lF) && lF < 480.0))
+        throw InvalidArg("samples >= 2^29 needs e^{beta max d} max|v| < 2^479");
+    const double lW = std::log2((double)W);
+    const int e1 = vmax > 0.0 ? std::min(1080, (int)std::floor(124.0 - lW - lF)) : 0;
+    const int e2 = vmax > 0.0 ? std::min(1080, (int)std::floor(125.0 - lW - 2.0 * lF)) : 0;
+    unsigned long long* acc1 = h->acc.get<unsigned long long>(4 * nrows);
+    unsigned long long* acc2 = acc1 + 2 * nrows;
+    CK(cudaMemsetAsync(acc1, 0, nrows * 32, s));
+    const uint64_t B = 1ull << 26;  // fixed (W >= 2^29), so repeated calls never regrow
+    uint32_t* row_of = h->row_of.get<uint32_t>(B);
+    for (uint64_t q0 = 0; q0 < J; q0 += B) {
+        const uint64_t q1 = std::min(J, q0 + B);
+        launch_expand_rows(off, nrows, q0, q1, row_of, s);
+        launch_entry_big_walk(h->m, rows_d, rowc, Kr, row_of, off, fp, q0, q1,
+                              std::ldexp(1.0, e1 - 64), std::ldexp(1.0, e2 - 64), acc1, acc2,
+                              jr, s);
+        after_launch(2);
+    }
+    launch_entry_big_fold(nrows, acc1, acc2, std::ldexp(1.0, -e1), std::ldexp(1.0, -e2), s1, s2,
+                          s);
+    after_launch(1);
+    launch_entry_big_finalize(nrows, W, Kr, s1, s2, jr, value, se, jumps, s);
+    after_launch(1);
+    CK(cudaGetLastError());
+}
+
 // Run the entry estimator for host rows / host v; outputs to host.
 void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* rows,
                  uint64_t nrows, const expmc_path_params* p, double* value, double* se,
@@ -481,8 +551,9 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
     } else if (nrows != n) {
         throw InvalidArg("rows == NULL requires nrows == n");
     }
-    if (fast && p->samples >= (1ull << 29))
-        throw InvalidArg("samples must be < 2^29 for the entry walker");
+    // W >= 2^29 walkers per entry: the grouped large-W path (K3 packs walker
+    // indices into 29 bits)
+    const bool big = fast && p->samples >= (1ull << 29);
     if (nrows == 0) return;
     DeviceGuard g(h->device);
     cudaStream_t s = h->stream;
@@ -529,6 +600,20 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
         double* ov = h->out_val.get<double>(nrows);
         double* os = h->out_se.get<double>(nrows);
         uint64_t* oj = h->out_j.get<uint64_t>(nrows);
+        if (big) {
+            run_entries_big(h, rd, nrows, p, ov, os, oj, s);
+            launch_sum_u64(nrows, oj, jtot, s);
+            after_launch(1);
+            unsigned long long res[2] = {0, 0};
+            CK(cudaMemcpyAsync(value, ov, nrows * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(se, os, nrows * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(jumps, oj, nrows * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(res, sc, 16, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if ((unsigned int)res[0]) throw InvalidArg("non-finite entry in v");
+            if (total_jumps) *total_jumps = res[1];
+            return;
+        }
         static const int env_pieces = [] {
             const char* e = getenv("EXPMC_PIECES");  // experiments only
             return e ? atoi(e) : 0;
@@ -1236,10 +1321,13 @@ int expmc_cuda_entries_device(expmc_matrix* h, const uint32_t* rows_dev, uint64_
         validate_params(p);
         if (p->rng != EXPMC_RNG_PHILOX)
             throw InvalidArg("entries_device supports the Philox walker only");
-        if (p->samples >= (1ull << 29))
-            throw InvalidArg("samples must be < 2^29 for the entry walker");
-        if (nrows >= (1ull << 30)) throw InvalidArg("at most 2^30 rows per call");
         DeviceGuard g(h->device);
+        if (p->samples >= (1ull << 29)) {  // large-W grouped path (synchronises the stream)
+            run_entries_big(h, rows_dev, nrows, p, value_dev, std_error_dev, jumps_dev,
+                            pick_stream(h, stream));
+            return;
+        }
+        if (nrows >= (1ull << 30)) throw InvalidArg("at most 2^30 rows per call");
         // scratch is owned by the handle: one stream per handle at a time
         void* scratch = h->part.get<unsigned char>(entry_fast_scratch_bytes(nrows, p->samples));
         const int k = launch_entry_fast(h->m, rows_dev, nrows, fast_params(p, p->samples),

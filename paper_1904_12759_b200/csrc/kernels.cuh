@@ -134,6 +134,26 @@ void launch_vec_walk(const DevSplit& m, const double2* rowc, const uint32_t* row
                      unsigned long long* part_j, cudaStream_t s);
 void launch_fixed_to_values(const unsigned long long* acc, uint64_t n, double inv_scale,
                             double* values, cudaStream_t s);
+// large-W entry path (samples >= 2^29)
+void launch_entry_big_rows(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
+                           const FastParams& p, uint64_t* jcount, double2* rowc, double* Kr,
+                           double* s1, double* s2, unsigned long long* jumps, cudaStream_t s);
+void launch_entry_big_walk(const DevSplit& m, const uint32_t* rows, const double2* rowc,
+                           const double* Kr, const uint32_t* row_of, const uint64_t* off,
+                           const FastParams& p, uint64_t q0, uint64_t q1, double sc1_hi,
+                           double sc2_hi, unsigned long long* acc1, unsigned long long* acc2,
+                           unsigned long long* jumps, cudaStream_t s);
+void launch_entry_big_fold(uint64_t nrows, const unsigned long long* acc1,
+                           const unsigned long long* acc2, double inv1, double inv2, double* s1,
+                           double* s2, cudaStream_t s);
+void launch_rec_v_absmax(const DevSplit& m, unsigned long long* out, cudaStream_t s);
+void launch_entry_big_finalize(uint64_t nrows, uint64_t W, const double* Kr, const double* s1,
+                               const double* s2, const unsigned long long* jumps, double* value,
+                               double* se, uint64_t* out_jumps, cudaStream_t s);
+// per-run sums of already sorted keys (scatter_sort.cu): out[key] += Σ run
+size_t run_sums_temp_bytes(uint64_t count);
+void run_sums_sorted(const uint32_t* keys, const double* vals, uint64_t count, void* temp,
+                     size_t temp_bytes, double* out, cudaStream_t s);
 void launch_binomial_debug(uint64_t n, double p, uint64_t count, const PhiloxKeys& K,
                            uint64_t* out, cudaStream_t s);
 

@@ -119,17 +119,30 @@ void scatter_sort_accumulate(uint32_t* end, double* f, uint32_t* end_sorted, dou
         throw std::runtime_error("scatter_sort: temp storage too small");
     cub::DeviceRadixSort::SortPairs(temp, tb, end, end_sorted, f, f_sorted, (int)count, 0,
                                     key_bits(n), s);
-    // piece buffers after the sort's temp storage
-    const uint64_t chunks = (count + kChunk - 1) / kChunk;
     const size_t sort_bytes = (tb + 255) & ~(size_t)255;
-    double* head = reinterpret_cast<double*>(static_cast<unsigned char*>(temp) + sort_bytes);
+    run_sums_sorted(end_sorted, f_sorted, count, static_cast<unsigned char*>(temp) + sort_bytes,
+                    temp_bytes - sort_bytes, values, s);
+}
+
+size_t run_sums_temp_bytes(uint64_t count) {
+    return 2 * ((count + kChunk - 1) / kChunk) * sizeof(double) + 256;
+}
+
+// out[key] += sum of each run of equal keys (keys sorted), in record order.
+void run_sums_sorted(const uint32_t* keys, const double* vals, uint64_t count, void* temp,
+                     size_t temp_bytes, double* out, cudaStream_t s) {
+    if (count == 0) return;
+    const uint64_t chunks = (count + kChunk - 1) / kChunk;
+    if (2 * chunks * sizeof(double) > temp_bytes)
+        throw std::runtime_error("run_sums: temp storage too small");
+    double* head = static_cast<double*>(temp);
     double* tail = head + chunks;
     cudaFuncSetAttribute(run_pieces_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kPieceSmem);  // per device; cheap
     run_pieces_kernel<<<(unsigned)((chunks + kPieceThreads - 1) / kPieceThreads), kPieceThreads,
-                        kPieceSmem, s>>>(end_sorted, f_sorted, count, head, tail, values);
-    run_spans_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, s>>>(end_sorted, count, head,
-                                                                      tail, values);
+                        kPieceSmem, s>>>(keys, vals, count, head, tail, out);
+    run_spans_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, s>>>(keys, count, head, tail,
+                                                                      out);
 }
 
 }  // namespace expmc_b200

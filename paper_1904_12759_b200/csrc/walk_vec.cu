@@ -40,6 +40,8 @@ namespace {
 constexpr uint32_t kTagTree = 0x4d554c54u;   // 'MULT' multinomial tree
 constexpr uint32_t kTagStay = 0x53544159u;   // 'STAY' never-jumper binomial
 constexpr uint32_t kTagDebug = 0x44454247u;  // 'DEBG' binomial test hook
+constexpr uint32_t kTagBig = 0x454c5247u;    // 'ELRG' large-W entry jumpers
+constexpr uint32_t kTagBigStay = 0x45535459u; // 'ESTY' large-W never-jumper split
 constexpr int kRowsThreads = 256;
 constexpr unsigned kRowsBlocks = 148 * 8;
 
@@ -235,30 +237,38 @@ __global__ void fixed_to_values_kernel(const unsigned long long* __restrict__ ac
     }
 }
 
-// row_of[q - q0] = the start row of jumper q, for q in [q0, q1).  Lane r of a
-// warp tests row (base + r); the warp then writes each overlapping row's
-// slice cooperatively (coalesced).
+// row_of[q - q0] = the start row of jumper q, for q in [q0, q1).  Each warp
+// owns chunks of 1024 consecutive jumpers: one binary search over the
+// offsets finds the row of the chunk's first jumper, then the warp walks
+// the rows forward writing each row's slice (coalesced).  Balanced for many
+// small rows and for a few rows with billions of jumpers alike.
 __global__ void expand_rows_kernel(const uint64_t* __restrict__ off, uint64_t n, uint64_t q0,
                                    uint64_t q1, uint32_t* __restrict__ row_of) {
+    constexpr uint64_t kSpan = 1024;
     const int lane = threadIdx.x & 31;
-    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    for (uint64_t base = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x - lane);
-         base < n; base += warps * 32) {
-        const uint64_t i = base + lane;
-        uint64_t a = 0, b = 0;
-        if (i < n) {
-            a = off[i];
-            b = off[i + 1];
-            a = a > q0 ? a : q0;
-            b = b < q1 ? b : q1;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t nchunks = (q1 - q0 + kSpan - 1) / kSpan;
+    for (uint64_t c = warp; c < nchunks; c += warps) {
+        const uint64_t c0 = q0 + c * kSpan;
+        const uint64_t c1 = c0 + kSpan < q1 ? c0 + kSpan : q1;
+        uint64_t r = 0;
+        if (lane == 0) {  // last r with off[r] <= c0 (upper_bound - 1)
+            uint64_t a = 0, b = n + 1;
+            while (a < b) {
+                const uint64_t mid = a + (b - a) / 2;
+                if (off[mid] <= c0) a = mid + 1; else b = mid;
+            }
+            r = a - 1;
         }
-        unsigned hit = __ballot_sync(0xffffffffu, a < b);
-        while (hit) {
-            const int src = __ffs(hit) - 1;
-            hit &= hit - 1;
-            const uint64_t sa = __shfl_sync(0xffffffffu, a, src);
-            const uint64_t sb = __shfl_sync(0xffffffffu, b, src);
-            for (uint64_t q = sa + lane; q < sb; q += 32) row_of[q - q0] = (uint32_t)(base + src);
+        r = __shfl_sync(0xffffffffu, r, 0);
+        uint64_t pos = c0;
+        while (pos < c1) {
+            uint64_t end = off[r + 1];
+            end = end < c1 ? end : c1;
+            for (uint64_t q = pos + lane; q < end; q += 32) row_of[q - q0] = (uint32_t)r;
+            pos = end > pos ? end : pos;
+            ++r;
         }
     }
 }
@@ -370,6 +380,231 @@ vec_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Entry estimator for W >= 2^29 walkers per entry (entry_estimate,
+// estimator.cpp:169-206, any `samples`): the K3 walker packs walker indices
+// into 29 bits, so very large W take this grouped path instead.  Per listed
+// row r (matrix row i = rows[r]): n0 = W - Binomial(W, 1 - e^{-λ_i})
+// never-jumpers score f0 = e^{β d_i} v_i; the jumpers (numbered q globally,
+// k = q - off[r] within the row) walk as vec_walk_kernel and score
+// w v_end.  Sums are kept as deviations from K_r (f0 when never-jumpers
+// are the majority, else 0 — K3's rule), so the never-jumpers add
+// n0 (f0 - K) and no variance cancels.  Jumper deviations and their squares
+// go to records in q order (= row order), summed per row by the
+// deterministic run-sum passes; jump counts by integer atomics.
+
+// rowc[r] = {1 - e^{-λ_i}, N / (β rate_i)}; rk[r] = {K_r, -}; s1/s2 start
+// with the never-jumpers' n0 (f0 - K), n0 (f0 - K)^2.
+__global__ void entry_big_rows_kernel(const uint32_t* __restrict__ rows, uint64_t nrows,
+                                      const RowRec* __restrict__ rec,
+                                      const double* __restrict__ rate, FastParams p,
+                                      uint64_t* __restrict__ jcount, double2* __restrict__ rowc,
+                                      double* __restrict__ Kr, double* __restrict__ s1,
+                                      double* __restrict__ s2,
+                                      unsigned long long* __restrict__ jumps) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < nrows;
+         r += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = rows[r];
+        const RowRec ri = load_rec(rec, i);
+        const double lam = __dmul_rn(rate[i], p.beta);
+        const double pj = -expm1(-lam);
+        const uint64_t J = binomial(p.W, pj, i, 0u, kTagBigStay, p.rk);
+        const uint64_t n0 = p.W - J;
+        const double f0 = __dmul_rn(exp(__dmul_rn(p.beta, ri.d)), ri.v);
+        const double K = pj <= 0.5 ? f0 : 0.0;  // e^{-λ} >= 1/2: never-jumpers dominate
+        const double c = __dsub_rn(f0, K);
+        rowc[r] = make_double2(pj, __ddiv_rn(p.inv_dt, rate[i]));
+        Kr[r] = K;
+        s1[r] = __dmul_rn((double)n0, c);
+        s2[r] = __dmul_rn(__dmul_rn((double)n0, c), c);
+        jcount[r] = J;
+        jumps[r] = 0ull;
+    }
+}
+
+struct U128 {
+    unsigned long long lo, hi;
+};
+
+__device__ __forceinline__ void add128(U128& a, U128 b) {
+    const unsigned long long lo = a.lo + b.lo;
+    a.hi += b.hi + (lo < a.lo ? 1ull : 0ull);
+    a.lo = lo;
+}
+
+// |x| 2^s as an unsigned 128-bit integer (x 2^(s-64) = y: hi = floor(y),
+// lo = frac(y) 2^64; power-of-2 scalings and the split are exact), then two's
+// complement for x < 0.
+__device__ __forceinline__ U128 to_fixed(double x, double scale_hi) {
+    const double y = __dmul_rn(fabs(x), scale_hi);
+    const double yh = floor(y);
+    U128 r{(unsigned long long)__dmul_rn(__dsub_rn(y, yh), 0x1.0p64), (unsigned long long)yh};
+    if (x < 0.0) {
+        r.lo = ~r.lo + 1ull;
+        r.hi = ~r.hi + (r.lo == 0ull ? 1ull : 0ull);
+    }
+    return r;
+}
+
+__device__ __forceinline__ void flush128(unsigned long long* __restrict__ acc, uint64_t r, U128 a) {
+    if ((a.lo | a.hi) == 0ull) return;
+    const unsigned long long old = atomicAdd(acc + 2 * r, a.lo);
+    const unsigned long long hi = a.hi + (old + a.lo < old ? 1ull : 0ull);
+    if (hi) atomicAdd(acc + 2 * r + 1, hi);
+}
+
+// Jumper walks of the large-W entry path.  Each lane keeps exact 128-bit
+// fixed-point sums of dev = f - K_r and dev^2 for the row its jumpers come
+// from (static grid-stride assignment: a lane's consecutive jumpers share a
+// row unless the stride crosses a row boundary) and flushes them with
+// integer atomics when the row changes: exact and order-independent, so
+// deterministic whatever the scheduling.
+__global__ void __launch_bounds__(128)
+entry_big_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj,
+                      const uint32_t* __restrict__ thr, const uint32_t* __restrict__ alias,
+                      const uint32_t* __restrict__ rows, const double2* __restrict__ rowc,
+                      const double* __restrict__ Kr, const uint32_t* __restrict__ row_of,
+                      const uint64_t* __restrict__ off, FastParams p, uint64_t q0, uint64_t q1,
+                      double sc1_hi, double sc2_hi, unsigned long long* __restrict__ acc1,
+                      unsigned long long* __restrict__ acc2,
+                      unsigned long long* __restrict__ jumps) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t q = q0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    bool active = false;
+    uint32_t r = 0, i = 0, off_c = 0, degf = 0, step = 0, jc = 0, klo = 0, tagv = 0;
+    float ir = 0.f;
+    double dcur = 0.0, vcur = 0.0, t = 0.0, S = 0.0, g = 0.0, corr0 = 0.0, K = 0.0;
+    uint32_t ar = 0xffffffffu;  // row of the lane's open sums
+    U128 a1{0, 0}, a2{0, 0};
+    unsigned long long aj = 0;
+    while (true) {
+        if (!active) {
+            if (q >= q1) break;
+            r = __ldg(row_of + (q - q0));
+            if (r != ar) {
+                if (ar != 0xffffffffu) {
+                    flush128(acc1, ar, a1);
+                    flush128(acc2, ar, a2);
+                    if (aj) atomicAdd(jumps + ar, aj);
+                }
+                ar = r;
+                a1 = U128{0, 0};
+                a2 = U128{0, 0};
+                aj = 0;
+            }
+            i = __ldg(rows + r);
+            K = __ldg(Kr + r);
+            const uint64_t k = q - __ldg(off + r);
+            klo = (uint32_t)k;
+            tagv = kTagBig ^ (uint32_t)(k >> 32);
+            const RowRec rs = load_rec(rec, i);
+            const double2 rc = __ldg(rowc + r);
+            const U4 w = philox4x32_10(U4{0u, klo, i, tagv}, p.rk);
+            const float u = __fmul_rn(__uint2float_rn(w.x >> 8) + 0.5f, 0x1.0p-24f);
+            const float R = -log1pf(-__fmul_rn(u, (float)rc.x));
+            double tn = __dmul_rn((double)R, rc.y);
+            if (!(tn < p.n_grid)) tn = __dmul_rn(p.n_grid, 1.0 - 0x1.0p-53);
+            corr0 = p.strang ? __dmul_rn(0.5, rs.d) : rs.d;
+            const double kk = ceil(tn);
+            S = __dmul_rn(rs.d, kk);
+            g = kk;
+            t = tn;
+            const Edge e = jump_edge(w.y, w.w, w.z, rs.off, rs.deg_flags, adj, thr, alias);
+            off_c = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d; vcur = e.v;
+            jc = 1;
+            step = 1;
+            active = true;
+        }
+        const U4 w = philox4x32_10(U4{step, klo, i, tagv}, p.rk);
+        const float h = __fmul_rn(neg_ln_u(w.x), ir);
+        const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
+        if (tn >= p.n_grid) {
+            S = __fma_rn(dcur, __dsub_rn(p.n_grid1, g), S);
+            // Strang: half weights at both ends; Lie: after-weights only
+            // (estimator.cpp:176-180) — K3's exponent
+            const double Sx = p.strang ? __dsub_rn(S, __dmul_rn(0.5, dcur)) : S;
+            const double f = __dmul_rn(exp(__dmul_rn(p.dt, __dsub_rn(Sx, corr0))), vcur);
+            const double dv = __dsub_rn(f, K);
+            add128(a1, to_fixed(dv, sc1_hi));
+            add128(a2, to_fixed(__dmul_rn(dv, dv), sc2_hi));
+            aj += jc;
+            active = false;
+            q += stride;
+        } else {
+            const double kk = ceil(tn);
+            S = __fma_rn(dcur, __dsub_rn(kk, g), S);
+            g = kk;
+            t = tn;
+            const Edge e = jump_edge(w.y, w.w, w.z, off_c, degf, adj, thr, alias);
+            off_c = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d; vcur = e.v;
+            ++jc;
+            ++step;
+        }
+    }
+    if (ar != 0xffffffffu) {
+        flush128(acc1, ar, a1);
+        flush128(acc2, ar, a2);
+        if (aj) atomicAdd(jumps + ar, aj);
+    }
+}
+
+// s1 += (signed 128-bit acc1) 2^-s1, s2 += acc2 2^-s2 (one rounding each)
+__global__ void entry_big_fold_kernel(uint64_t nrows, const unsigned long long* __restrict__ acc1,
+                                      const unsigned long long* __restrict__ acc2,
+                                      double inv1, double inv2, double* __restrict__ s1,
+                                      double* __restrict__ s2) {
+    const uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (r >= nrows) return;
+    unsigned long long lo = acc1[2 * r], hi = acc1[2 * r + 1];
+    const bool neg = (long long)hi < 0;
+    if (neg) {
+        lo = ~lo + 1ull;
+        hi = ~hi + (lo == 0ull ? 1ull : 0ull);
+    }
+    double x = __fma_rn(__ull2double_rn(hi), 0x1.0p64, __ull2double_rn(lo));
+    x = __dmul_rn(neg ? -x : x, inv1);
+    s1[r] = __dadd_rn(s1[r], x);
+    const double y = __fma_rn(__ull2double_rn(acc2[2 * r + 1]), 0x1.0p64,
+                              __ull2double_rn(acc2[2 * r]));
+    s2[r] = __dadd_rn(s2[r], __dmul_rn(y, inv2));
+}
+
+// max |v| over the packed row records (bit patterns of non-negative doubles
+// order like unsigned integers)
+__global__ void rec_v_absmax_kernel(const RowRec* __restrict__ rec, uint64_t n,
+                                    unsigned long long* __restrict__ out) {
+    unsigned long long m = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        m = max(m, (unsigned long long)__double_as_longlong(fabs(rec[i].v)));
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// value = K + Σdev / W, SE from the one-pass variance of the deviations
+// clamped at 0 (finalize, estimator.cpp:76-89).
+__global__ void entry_big_finalize_kernel(uint64_t nrows, uint64_t W,
+                                          const double* __restrict__ Kr,
+                                          const double* __restrict__ s1,
+                                          const double* __restrict__ s2,
+                                          const unsigned long long* __restrict__ jumps,
+                                          double* __restrict__ value, double* __restrict__ se,
+                                          uint64_t* __restrict__ out_jumps) {
+    const uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (r >= nrows) return;
+    const double mm = (double)W;
+    value[r] = __dadd_rn(Kr[r], __ddiv_rn(s1[r], mm));
+    double e = 0.0;
+    if (W > 1) {
+        const double var =
+            fmax(0.0, __ddiv_rn(__dsub_rn(s2[r], __ddiv_rn(__dmul_rn(s1[r], s1[r]), mm)),
+                                __dsub_rn(mm, 1.0)));
+        e = sqrt(__ddiv_rn(var, mm));
+    }
+    se[r] = e;
+    out_jumps[r] = jumps[r];
+}
+
 __global__ void binomial_debug_kernel(uint64_t n, double p, uint64_t count, PhiloxKeys K,
                                       uint64_t* __restrict__ out) {
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < count;
@@ -421,8 +656,9 @@ void launch_scan_u64(const uint64_t* in, uint64_t* out, uint64_t count, void* te
 
 void launch_expand_rows(const uint64_t* off, uint64_t n, uint64_t q0, uint64_t q1,
                         uint32_t* row_of, cudaStream_t s) {
-    const uint64_t warps = (n + 31) / 32;
-    const unsigned blocks = (unsigned)std::min<uint64_t>((warps + 7) / 8, 148 * 16);
+    if (q1 <= q0) return;
+    const uint64_t chunks = (q1 - q0 + 1023) / 1024;  // one warp per chunk, 8 per block
+    const unsigned blocks = (unsigned)std::min<uint64_t>((chunks + 7) / 8, 148 * 16);
     expand_rows_kernel<<<blocks, 256, 0, s>>>(off, n, q0, q1, row_of);
 }
 
@@ -440,6 +676,43 @@ void launch_vec_walk(const DevSplit& m, const double2* rowc, const uint32_t* row
 void launch_fixed_to_values(const unsigned long long* acc, uint64_t n, double inv_scale,
                             double* values, cudaStream_t s) {
     fixed_to_values_kernel<<<148 * 8, 256, 0, s>>>(acc, n, inv_scale, values);
+}
+
+void launch_entry_big_rows(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
+                           const FastParams& p, uint64_t* jcount, double2* rowc, double* Kr,
+                           double* s1, double* s2, unsigned long long* jumps, cudaStream_t s) {
+    const unsigned blocks = (unsigned)std::min<uint64_t>((nrows + 255) / 256, 148 * 8);
+    entry_big_rows_kernel<<<blocks ? blocks : 1, 256, 0, s>>>(rows, nrows, m.rec, m.rate, p,
+                                                               jcount, rowc, Kr, s1, s2, jumps);
+}
+
+void launch_entry_big_walk(const DevSplit& m, const uint32_t* rows, const double2* rowc,
+                           const double* Kr, const uint32_t* row_of, const uint64_t* off,
+                           const FastParams& p, uint64_t q0, uint64_t q1, double sc1_hi,
+                           double sc2_hi, unsigned long long* acc1, unsigned long long* acc2,
+                           unsigned long long* jumps, cudaStream_t s) {
+    entry_big_walk_kernel<<<vec_walk_grid(), 128, 0, s>>>(m.rec, m.adj, m.alias_thr,
+                                                          m.alias_idx, rows, rowc, Kr, row_of,
+                                                          off, p, q0, q1, sc1_hi, sc2_hi, acc1,
+                                                          acc2, jumps);
+}
+
+void launch_entry_big_fold(uint64_t nrows, const unsigned long long* acc1,
+                           const unsigned long long* acc2, double inv1, double inv2, double* s1,
+                           double* s2, cudaStream_t s) {
+    entry_big_fold_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(nrows, acc1, acc2,
+                                                                          inv1, inv2, s1, s2);
+}
+
+void launch_rec_v_absmax(const DevSplit& m, unsigned long long* out, cudaStream_t s) {
+    rec_v_absmax_kernel<<<148 * 4, 256, 0, s>>>(m.rec, m.n, out);
+}
+
+void launch_entry_big_finalize(uint64_t nrows, uint64_t W, const double* Kr, const double* s1,
+                               const double* s2, const unsigned long long* jumps, double* value,
+                               double* se, uint64_t* out_jumps, cudaStream_t s) {
+    entry_big_finalize_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(
+        nrows, W, Kr, s1, s2, jumps, value, se, out_jumps);
 }
 
 void launch_binomial_debug(uint64_t n, double p, uint64_t count, const PhiloxKeys& K,

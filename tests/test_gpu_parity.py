@@ -495,10 +495,13 @@ def test_philox_walker_gap_edge_cases(pb, orc, graphs, W):
         assert np.array_equal(got.jumps, mj), beta
 
 
-def test_entry_walker_sample_limit(pb, graphs):
+def test_entry_walker_large_samples_window(pb, graphs):
+    """samples >= 2^29 runs the grouped large-W path (tests/test_gpu_vector.py);
+    its exact fixed-point sums need the weights inside a 2^479 window, and it
+    says so instead of overflowing."""
     m = pb.split(graphs["p3"])
-    p = pb.PathParams(1.0, 8, 1 << 29, pb.Splitting.Strang, 1, pb.Rng.PHILOX)
-    with pytest.raises(ValueError, match="samples must be < 2\\^29 for the entry walker"):
+    p = pb.PathParams(400.0, 8, 1 << 29, pb.Splitting.Strang, 1, pb.Rng.PHILOX)
+    with pytest.raises(ValueError, match="samples >= 2\\^29 needs"):
         pb.entries_estimate(m, np.ones(3), np.array([0], np.uint32), p)
 
 

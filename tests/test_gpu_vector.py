@@ -296,3 +296,39 @@ def test_fixed_point_falls_back_on_wide_weight_range(pb, ref):
                                                              workers=16)
     z = (got.values.sum() - rv.sum()) / math.sqrt(got.std_error_global ** 2 + rse ** 2)
     assert abs(z) < 4.0
+
+
+@pytest.mark.parametrize("splitting", [0, 1])
+def test_entries_beyond_2_29_walkers(pb, splitting):
+    """entry_estimate accepts any `samples` (estimator.hpp:19): W >= 2^29
+    takes the grouped large-W path.  Against the K3 walker just below the
+    threshold (same law) and against the splitting product x (the exact mean)
+    within 5 combined SE; signed v, rows with never-jumper majority (K = f0)
+    and with jumper majority (K = 0)."""
+    a = np.zeros((6, 6))
+    for i, j, w in [(0, 1, 1.0), (1, 2, 2.0), (2, 3, 0.5), (3, 4, 3.0), (4, 5, 1.0), (0, 5, 0.25)]:
+        a[i, j] = a[j, i] = w
+    np.fill_diagonal(a, [0.1, -0.3, 0.2, 0.0, -0.1, 0.4])
+    csr = pb.csr_from_dense(a)
+    m = pb.split(csr)
+    v = np.array([1.0, -0.5, 2.0, 0.3, -1.2, 0.7])
+    beta = 0.2   # λ from 0.05 (row 0: K = f0) to 0.8 (row 3: K = 0)
+    rows = np.arange(6, dtype=np.uint32)
+    big = pb.entries_estimate(m, v, rows, pb.PathParams(beta, 16, 1 << 29, pb.Splitting(splitting), 7))
+    Ws = 1 << 25  # K3 (the threshold's other side; few rows => slow at 2^29 - 1)
+    small = pb.entries_estimate(m, v, rows, pb.PathParams(beta, 16, Ws, pb.Splitting(splitting), 8))
+    x = pb.splitting_product(m, v, pb.PathParams(beta, 16, 10, pb.Splitting(splitting)))
+    assert np.all(big.std_errors > 0)
+    z = (big.values - small.values) / np.sqrt(big.std_errors ** 2 + small.std_errors ** 2)
+    assert np.all(np.abs(z) < 5), z
+    zx = (big.values - x) / big.std_errors
+    assert np.all(np.abs(zx) < 5), zx
+    # jump counts: same law as K3's (mean jumps per walker)
+    jb, js = big.jumps / float(1 << 29), small.jumps / float(Ws)
+    assert np.all(np.abs(jb - js) < 6 * np.sqrt(2.0 * np.maximum(js, 1e-9) / Ws) + 1e-12)
+    # the single-entry call routes the same way: the same walkers (keyed by
+    # row and walker), summed with a different piece alignment
+    e = pb.entry_estimate(m, v, 3, pb.PathParams(beta, 16, 1 << 29, pb.Splitting(splitting), 7))
+    assert e.total_jumps == big.jumps[3]
+    assert e.value == pytest.approx(big.values[3], rel=1e-11)
+    assert e.std_error == pytest.approx(big.std_errors[3], rel=1e-9)
