@@ -332,3 +332,27 @@ def test_entries_beyond_2_29_walkers(pb, splitting):
     assert e.total_jumps == big.jumps[3]
     assert e.value == pytest.approx(big.values[3], rel=1e-11)
     assert e.std_error == pytest.approx(big.std_errors[3], rel=1e-9)
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 33, 1000])
+def test_small_sample_counts(pb, ref, M):
+    """Tiny M (down to one walker): the start tree, the never-jumper split
+    and the jumper batches handle empty rows and empty batches; tallies obey
+    finalize (SE 0 for M = 1)."""
+    from test_gpu_parity import _graphs
+
+    csr = _graphs(pb)["weighted_40"]
+    m = pb.split(csr)
+    v = pb.gen_vector(0, csr.n, 6)
+    v[[0, -1]] = 0.0  # zero mass at both ends of the cumulative table
+    p = pb.PathParams(0.5, 16, M, pb.Splitting.Strang, 3)
+    r = pb.vector_estimate(m, v, p)
+    assert np.all(np.isfinite(r.values)) and r.samples_used == M
+    assert r.values[0] >= 0 and (r.values > 0).sum() <= M
+    # Σ values = mean of V w over the M walkers, whose SE is std_error_global
+    if M == 1:
+        assert r.std_error_global == 0.0
+    t = pb.tc_estimate(m, p)
+    assert np.isfinite(t.value) and t.samples_used == M
+    c = pb.start_counts(m, v, M, seed=3)
+    assert c.sum() == M and c[0] == 0 and c[-1] == 0
