@@ -791,8 +791,10 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
         launch_expand_rows(off, n, q0, q1, row_of, s);
         launch_vec_walk(h->m, rowc, row_of, fp, v_sum, q0, q1, rec_end, rec_f, acc,
                         std::ldexp(1.0, scale_exp - 64), pa, pb, pc, s);
-        launch_final_reduce(pa, pb, pc, wparts, tot, tot + 1,
-                            reinterpret_cast<unsigned long long*>(tot + 2), s);
+        // batch tallies added to the running totals on the device, in batch
+        // order (the same fp sequence as adding them on the host)
+        launch_final_reduce_acc(pa, pb, pc, wparts, tot, tot + 1,
+                                reinterpret_cast<unsigned long long*>(tot + 2), s);
         after_launch(3);
         if (vals && !acc) {
             scatter_sort_accumulate(rec_end, rec_f, end_sorted, f_sorted, q1 - q0, n, temp,
@@ -800,14 +802,12 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
             after_launch(3);
             CK(cudaGetLastError());
         }
-        CK(cudaMemcpyAsync(res, tot, sizeof(res), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        uint64_t j;
-        std::memcpy(&j, &res[2], 8);
-        sum += res[0];
-        sq += res[1];
-        jumps += j;
     }
+    CK(cudaMemcpyAsync(res, tot, sizeof(res), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::memcpy(&jumps, &res[2], 8);
+    sum = res[0];
+    sq = res[1];
     CK(cudaGetLastError());
     if (acc) {
         launch_fixed_to_values(acc, n, std::ldexp(1.0, -scale_exp), vals, s);

@@ -161,6 +161,10 @@ void launch_binomial_debug(uint64_t n, double p, uint64_t count, const PhiloxKey
 void launch_final_reduce(const double* part_a, const double* part_b,
                          const unsigned long long* part_c, unsigned nparts, double* out_a,
                          double* out_b, unsigned long long* out_c, cudaStream_t s);
+// same, added to the running totals out_* (deterministic: launch order)
+void launch_final_reduce_acc(const double* part_a, const double* part_b,
+                             const unsigned long long* part_c, unsigned nparts, double* out_a,
+                             double* out_b, unsigned long long* out_c, cudaStream_t s);
 void launch_scale(uint64_t n, double* x, double alpha, cudaStream_t s);
 void launch_count_nonfinite(uint64_t n, const double* x, unsigned int* flag, cudaStream_t s);
 void launch_sum_u64(uint64_t n, const uint64_t* x, unsigned long long* out, cudaStream_t s);

@@ -11,7 +11,7 @@ __global__ void __launch_bounds__(256)
 final_reduce_kernel(const double* __restrict__ a, const double* __restrict__ b,
                     const unsigned long long* __restrict__ c, unsigned nparts,
                     double* __restrict__ oa, double* __restrict__ ob,
-                    unsigned long long* __restrict__ oc) {
+                    unsigned long long* __restrict__ oc, bool accumulate) {
     __shared__ double sa[256], sb[256];
     __shared__ unsigned long long sc[256];
     double x = 0.0, y = 0.0;
@@ -33,10 +33,10 @@ final_reduce_kernel(const double* __restrict__ a, const double* __restrict__ b,
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        *oa = sa[0];
-        *ob = sb[0];
-        *oc = sc[0];
+    if (threadIdx.x == 0) {  // accumulate: running totals added in launch order
+        *oa = accumulate ? __dadd_rn(*oa, sa[0]) : sa[0];
+        *ob = accumulate ? __dadd_rn(*ob, sb[0]) : sb[0];
+        *oc = accumulate ? *oc + sc[0] : sc[0];
     }
 }
 
@@ -81,7 +81,15 @@ void launch_count_nonfinite(uint64_t n, const double* x, unsigned int* flag, cud
 void launch_final_reduce(const double* part_a, const double* part_b,
                          const unsigned long long* part_c, unsigned nparts, double* out_a,
                          double* out_b, unsigned long long* out_c, cudaStream_t s) {
-    final_reduce_kernel<<<1, 256, 0, s>>>(part_a, part_b, part_c, nparts, out_a, out_b, out_c);
+    final_reduce_kernel<<<1, 256, 0, s>>>(part_a, part_b, part_c, nparts, out_a, out_b, out_c,
+                                          false);
+}
+
+void launch_final_reduce_acc(const double* part_a, const double* part_b,
+                             const unsigned long long* part_c, unsigned nparts, double* out_a,
+                             double* out_b, unsigned long long* out_c, cudaStream_t s) {
+    final_reduce_kernel<<<1, 256, 0, s>>>(part_a, part_b, part_c, nparts, out_a, out_b, out_c,
+                                          true);
 }
 
 void launch_scale(uint64_t n, double* x, double alpha, cudaStream_t s) {
