@@ -119,6 +119,8 @@ __device__ uint64_t binomial(uint64_t n, double p, uint32_t id0, uint32_t id1, u
     return flip ? n - x : x;
 }
 
+__global__ void set_root_kernel(uint64_t* cnt, uint64_t M) { cnt[0] = M; }
+
 // One level of the multinomial tree.  Node k of level L covers rows
 // [k << (D-L), (k+1) << (D-L)) ∩ [0, n); its count lives at cnt[lo] and its
 // right child's at cnt[mid] (zero until written here).
@@ -621,13 +623,13 @@ unsigned vec_walk_grid() { return 148 * 12; }
 int launch_start_counts(uint64_t n, uint64_t M, const double* cum, const PhiloxKeys& K,
                         uint64_t* cnt, cudaStream_t s) {
     cudaMemsetAsync(cnt, 0, n * 8, s);
-    cudaMemcpyAsync(cnt, &M, 8, cudaMemcpyHostToDevice, s);  // pageable: staged synchronously
+    set_root_kernel<<<1, 1, 0, s>>>(cnt, M);
     const int D = tree_depth(n);
-    for (int L = 0; L < D; ++L) {
+    for (int L = 0; L < D; ++L) {  // (returns D + 1 launches with the root)
         const uint64_t nodes = 1ull << L;
         tree_level_kernel<<<(unsigned)((nodes + 255) / 256), 256, 0, s>>>(cnt, n, D, L, cum, K);
     }
-    return D;
+    return D + 1;
 }
 
 void launch_vec_rows(const DevSplit& m, const uint64_t* cnt, const FastParams& p, double v_sum,
