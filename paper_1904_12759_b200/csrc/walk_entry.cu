@@ -63,6 +63,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef ENTRY_CARVE
 #define ENTRY_CARVE 1     // size the smem carveout for ENTRY_MIN_BLOCKS (max L1)
 #endif
+#ifndef ENTRY_DYNAMIC
+#define ENTRY_DYNAMIC 1 // tasks after the first grid-full from a global counter (0: static stride)
+#endif
 #ifndef ENTRY_POP_MIN
 #define ENTRY_POP_MIN 2 // run the scheduler once this many lanes are idle
 #endif
@@ -117,7 +120,8 @@ __global__ void __launch_bounds__(128, ENTRY_MIN_BLOCKS)
 entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rate,
                   const Edge* __restrict__ adj, const uint32_t* __restrict__ thr,
                   const uint32_t* __restrict__ alias, const uint32_t* __restrict__ rows,
-                  uint64_t nrows, FastParams p, double4* __restrict__ partial) {
+                  uint64_t nrows, FastParams p, double4* __restrict__ partial,
+                  unsigned int* __restrict__ task_ctr) {
     constexpr int RT = ENTRY_TASKS;
     constexpr uint32_t CAP = ENTRY_CAP;
     static_assert((RT & (RT - 1)) == 0 && RT <= 8 && (CAP & (CAP - 1)) == 0 && CAP >= kRound,
@@ -185,6 +189,19 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         }
     };
 
+    // Next task for this warp: static stride, or (ENTRY_DYNAMIC) the next
+    // unclaimed task after the first grid-full.  The result contract does
+    // not depend on which warp runs a task.
+    auto next_task = [&]() -> uint32_t {
+#if ENTRY_DYNAMIC
+        uint32_t t = 0;
+        if (lane == 0) t = tstride + atomicAdd(task_ctr, 1u);
+        return __shfl_sync(FULL, t, 0);
+#else
+        return atask + tstride;
+#endif
+    };
+
     // Open task `atask` in slot tw: row constants computed by two lanes in
     // parallel (lane 0: e^{-λ}, lane 1: e^{β d}).  Part w of a row owns the
     // walkers [⌊wW/WPR⌋, ⌊(w+1)W/WPR⌋).
@@ -224,7 +241,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         around = 0;
         atstart = tail;
         if (dead) {
-            atask += tstride;
+            atask = next_task();
         } else {
             aopen = true;
         }
@@ -298,7 +315,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 oend = tail;
             }
             aopen = false;
-            atask += tstride;
+            atask = next_task();
         }
         __syncwarp();
     };
@@ -533,8 +550,12 @@ int launch_t(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const Fast
     const uint64_t blocks = (warps + 3) / 4;
     const uint64_t cap = (uint64_t)nsm * ENTRY_MIN_BLOCKS;
     const unsigned grid = (unsigned)(blocks < cap ? blocks : cap);
+    unsigned int* ctr = reinterpret_cast<unsigned int*>(partial + warps);
+#if ENTRY_DYNAMIC
+    cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s);
+#endif
     entry_walk_kernel<WPR><<<grid, 128, pad, s>>>(m.rec, m.rate, m.adj, m.alias_thr, m.alias_idx,
-                                                rows, nrows, p, partial);
+                                                rows, nrows, p, partial, ctr);
     combine_parts_kernel<WPR><<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(
         partial, nrows, p.W, value, se, jumps);
     return 2;
@@ -549,7 +570,8 @@ int entry_fast_wpr(uint64_t W) {
 }
 
 size_t entry_fast_scratch_bytes(uint64_t nrows, uint64_t W) {
-    return nrows * (size_t)entry_fast_wpr(W) * sizeof(double4);
+    // per-task partials, then the task counter (ENTRY_DYNAMIC)
+    return nrows * (size_t)entry_fast_wpr(W) * sizeof(double4) + 256;
 }
 
 int launch_entry_fast(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
