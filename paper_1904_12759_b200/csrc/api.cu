@@ -513,7 +513,7 @@ void run_entries_big(expmc_matrix* h, const uint32_t* rows_d, uint64_t nrows,
     unsigned long long* acc1 = h->acc.get<unsigned long long>(4 * nrows);
     unsigned long long* acc2 = acc1 + 2 * nrows;
     CK(cudaMemsetAsync(acc1, 0, nrows * 32, s));
-    const uint64_t B = 1ull << 26;  // fixed (W >= 2^29), so repeated calls never regrow
+    const uint64_t B = 1ull << 28;  // fixed (W >= 2^29), so repeated calls never regrow
     uint32_t* row_of = h->row_of.get<uint32_t>(B);
     for (uint64_t q0 = 0; q0 < J; q0 += B) {
         const uint64_t q1 = std::min(J, q0 + B);
@@ -745,8 +745,6 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
     h->last_jumpers = J;
     // batch buffers sized by M (>= J), not by the random J, so repeated calls
     // with the same M never regrow (and re-allocate) them
-    const uint64_t B = std::min<uint64_t>(M, 1ull << 26);
-    uint32_t* row_of = h->row_of.get<uint32_t>(B);
     uint32_t *rec_end = nullptr, *end_sorted = nullptr;
     double *rec_f = nullptr, *f_sorted = nullptr;
     void* temp = nullptr;
@@ -778,6 +776,10 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
         }
         h->last_fixed = fits ? 1 : 0;
     }
+    // batches of 2^26 jumpers when (end, f) records are kept (sort path),
+    // else 2^28 (only the 4-byte start rows per jumper): fewer batch tails
+    const uint64_t B = std::min<uint64_t>(M, (vals && !acc) ? 1ull << 26 : 1ull << 28);
+    uint32_t* row_of = h->row_of.get<uint32_t>(B);
     if (vals && !acc) {
         rec_end = h->tmp1.get<uint32_t>(B * 2);
         end_sorted = rec_end + B;
