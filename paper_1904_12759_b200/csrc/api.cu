@@ -715,8 +715,9 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
     uint64_t* off = h->joff.get<uint64_t>(n + 1);
     const int levels = launch_start_counts(n, M, vcum, fp.rk, cnt, s);
     after_launch(levels);
-    const unsigned rparts = vec_rows_grid(), wparts = vec_walk_grid();
-    const unsigned parts = std::max(rparts, wparts);
+    const unsigned rparts = vec_rows_grid();
+    // walk tally parts: one per block of the largest batch (B <= 2^28)
+    const unsigned parts = std::max(rparts, vec_walk_blocks(std::min<uint64_t>(M, 1ull << 28)));
     double* pa = h->pa.get<double>(parts);
     double* pb = h->pb.get<double>(parts);
     unsigned long long* pc = h->pc.get<unsigned long long>(parts);
@@ -795,7 +796,7 @@ void run_grouped(expmc_matrix* h, const double* vcum, double v_sum, const expmc_
                         std::ldexp(1.0, scale_exp - 64), pa, pb, pc, s);
         // batch tallies added to the running totals on the device, in batch
         // order (the same fp sequence as adding them on the host)
-        launch_final_reduce_acc(pa, pb, pc, wparts, tot, tot + 1,
+        launch_final_reduce_acc(pa, pb, pc, vec_walk_blocks(q1 - q0), tot, tot + 1,
                                 reinterpret_cast<unsigned long long*>(tot + 2), s);
         after_launch(3);
         if (vals && !acc) {

@@ -115,7 +115,8 @@ void launch_gather_ceiling(const DevSplit& m, const uint32_t* rows, uint64_t nro
 
 // walk_vec.cu (K4: vector / tc by grouped starts)
 unsigned vec_rows_grid();
-unsigned vec_walk_grid();
+// walk kernels: blocks for a batch of `count` jumpers (one tally part each)
+unsigned vec_walk_blocks(uint64_t count);
 // returns the number of kernels launched (root + tree levels)
 int launch_start_counts(uint64_t n, uint64_t M, const double* cum, const PhiloxKeys& K,
                         uint64_t* cnt, cudaStream_t s);

@@ -6,6 +6,8 @@ namespace expmc_b200 {
 
 namespace {
 
+constexpr uint32_t kChainsPerThread = 16;
+
 // K6: memory-only walker with the K3 access pattern (neighbour id gather ->
 // landing record gather) and a cheap integer hash instead of Philox / log /
 // exp.  chains_per_row chains of chain_len jumps start at every listed row;
@@ -17,9 +19,13 @@ gather_ceiling_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ a
                       uint32_t chains_per_row, uint32_t chain_len, uint32_t salt,
                       unsigned long long* __restrict__ sink) {
     const uint64_t total = nrows * (uint64_t)chains_per_row;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    // block-owned chain ranges (many small blocks, balanced by the hardware
+    // block scheduler — the same work distribution as the K3/K4 walkers)
+    const uint64_t base = blockIdx.x * (uint64_t)blockDim.x * kChainsPerThread;
+    const uint64_t end = base + (uint64_t)blockDim.x * kChainsPerThread < total
+                             ? base + (uint64_t)blockDim.x * kChainsPerThread : total;
     unsigned long long acc = 0;
-    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < total; c += stride) {
+    for (uint64_t c = base + threadIdx.x; c < end; c += blockDim.x) {
         uint32_t cur = rows[c / chains_per_row];
         const RowRec r = load_rec(rec, cur);  // start record, as K3
         uint32_t off = r.off, degf = r.deg_flags;
@@ -43,8 +49,10 @@ void launch_gather_ceiling(const DevSplit& m, const uint32_t* rows, uint64_t nro
                            uint32_t chains_per_row, uint32_t chain_len, uint32_t salt,
                            unsigned long long* sink, cudaStream_t s) {
     if (nrows == 0 || chains_per_row == 0) return;
-    gather_ceiling_kernel<<<148 * 16, 128, 0, s>>>(m.rec, m.adj, rows, nrows,
-                                                  chains_per_row, chain_len, salt, sink);
+    const uint64_t total = nrows * (uint64_t)chains_per_row;
+    const uint64_t blocks = (total + 128ull * kChainsPerThread - 1) / (128ull * kChainsPerThread);
+    gather_ceiling_kernel<<<(unsigned)blocks, 128, 0, s>>>(m.rec, m.adj, rows, nrows,
+                                                          chains_per_row, chain_len, salt, sink);
 }
 
 }  // namespace expmc_b200

@@ -43,6 +43,7 @@ constexpr uint32_t kTagDebug = 0x44454247u;  // 'DEBG' binomial test hook
 constexpr uint32_t kTagBig = 0x454c5247u;    // 'ELRG' large-W entry jumpers
 constexpr uint32_t kTagBigStay = 0x45535459u; // 'ESTY' large-W never-jumper split
 constexpr int kRowsThreads = 256;
+constexpr uint32_t kPer = 64;  // jumpers per thread in the walk kernels
 constexpr unsigned kRowsBlocks = 148 * 8;
 
 __device__ __forceinline__ double u53(uint32_t hi, uint32_t lo) {
@@ -320,8 +321,14 @@ vec_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj,
                 unsigned long long* __restrict__ part_j) {
     __shared__ double sh1[4], sh2[4];
     __shared__ unsigned long long shj[4];
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t q = q0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    // block b owns jumpers [q0 + b T kPer, q0 + (b+1) T kPer): many small
+    // blocks, so the hardware block scheduler balances the SMs (a static
+    // grid-stride left SMs idle at the tail)
+    const uint64_t stride = blockDim.x;
+    const uint64_t qb0 = q0 + blockIdx.x * (uint64_t)blockDim.x * kPer;
+    const uint64_t qend = qb0 + (uint64_t)blockDim.x * kPer < q1 ? qb0 + (uint64_t)blockDim.x * kPer : q1;
+    uint64_t q = qb0 + threadIdx.x;
+    q1 = qend;
     double s1 = 0.0, s2 = 0.0;
     unsigned long long jt = 0;
     bool active = false;
@@ -465,8 +472,11 @@ entry_big_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ a
                       double sc1_hi, double sc2_hi, unsigned long long* __restrict__ acc1,
                       unsigned long long* __restrict__ acc2,
                       unsigned long long* __restrict__ jumps) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t q = q0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = blockDim.x;  // block-owned ranges, as vec_walk_kernel
+    const uint64_t qb0 = q0 + blockIdx.x * (uint64_t)blockDim.x * kPer;
+    const uint64_t qend = qb0 + (uint64_t)blockDim.x * kPer < q1 ? qb0 + (uint64_t)blockDim.x * kPer : q1;
+    uint64_t q = qb0 + threadIdx.x;
+    q1 = qend;
     bool active = false;
     uint32_t r = 0, i = 0, off_c = 0, degf = 0, step = 0, jc = 0, klo = 0, tagv = 0;
     float ir = 0.f;
@@ -618,7 +628,10 @@ int tree_depth(uint64_t n) {
 }  // namespace
 
 unsigned vec_rows_grid() { return kRowsBlocks; }
-unsigned vec_walk_grid() { return 148 * 12; }
+unsigned vec_walk_blocks(uint64_t count) {
+    const uint64_t b = (count + 128ull * kPer - 1) / (128ull * kPer);
+    return (unsigned)(b ? b : 1);
+}
 
 int launch_start_counts(uint64_t n, uint64_t M, const double* cum, const PhiloxKeys& K,
                         uint64_t* cnt, cudaStream_t s) {
@@ -664,7 +677,7 @@ void launch_vec_walk(const DevSplit& m, const double2* rowc, const uint32_t* row
                      uint32_t* out_end, double* out_f, unsigned long long* acc,
                      double scale_hi, double* part_s1, double* part_s2,
                      unsigned long long* part_j, cudaStream_t s) {
-    vec_walk_kernel<<<vec_walk_grid(), 128, 0, s>>>(m.rec, m.adj, m.alias_thr, m.alias_idx,
+    vec_walk_kernel<<<vec_walk_blocks(q1 - q0), 128, 0, s>>>(m.rec, m.adj, m.alias_thr, m.alias_idx,
                                                     rowc, row_of, p, v_sum, q0, q1, out_end,
                                                     out_f, acc, scale_hi, part_s1, part_s2,
                                                     part_j);
@@ -688,7 +701,7 @@ void launch_entry_big_walk(const DevSplit& m, const uint32_t* rows, const double
                            const FastParams& p, uint64_t q0, uint64_t q1, double sc1_hi,
                            double sc2_hi, unsigned long long* acc1, unsigned long long* acc2,
                            unsigned long long* jumps, cudaStream_t s) {
-    entry_big_walk_kernel<<<vec_walk_grid(), 128, 0, s>>>(m.rec, m.adj, m.alias_thr,
+    entry_big_walk_kernel<<<vec_walk_blocks(q1 - q0), 128, 0, s>>>(m.rec, m.adj, m.alias_thr,
                                                           m.alias_idx, rows, rowc, Kr, row_of,
                                                           off, p, q0, q1, sc1_hi, sc2_hi, acc1,
                                                           acc2, jumps);
