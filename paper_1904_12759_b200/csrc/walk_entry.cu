@@ -66,9 +66,25 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef ENTRY_DYNAMIC
 #define ENTRY_DYNAMIC 1 // tasks after the first grid-full from a global counter (0: static stride)
 #endif
+#ifndef ENTRY_SWZ
+#define ENTRY_SWZ 0 // 1: swizzle the ticket ring (measured 1.5% slower: the conflicts are not the limiter)
+#endif
 #ifndef ENTRY_POP_MIN
 #define ENTRY_POP_MIN 2 // run the scheduler once this many lanes are idle
 #endif
+
+// Physical slot of ticket position `pos` in the tk ring.  A gap round
+// stores ticket (lane, k) at tail + 4 lane + k: 8-byte slots 32 bytes apart
+// hit 4 bank pairs (8-way conflicts).  XOR-ing bits 4-5 into bits 0-1
+// spreads them over 16 bank pairs; consecutive positions (pops, batches)
+// stay conflict-free, and the sink slot CAP maps to itself (CAP % 64 == 0).
+__device__ __forceinline__ uint32_t tk_slot(uint32_t pos) {
+#if ENTRY_SWZ
+    return pos ^ ((pos >> 4) & 3u);
+#else
+    return pos;
+#endif
+}
 
 struct RowRecU {     // RowRec without its 32-byte alignment (smem copy)
     uint32_t off, deg_flags;
@@ -177,7 +193,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             const uint32_t pos = tk & (CAP - 1);
             q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, DCUR)) : S;
             q.v[pos] = VCUR;
-            q.tk[pos].x = jc;
+            q.tk[tk_slot(pos)].x = jc;
             act = false;
             fin = true;
         } else {
@@ -299,7 +315,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             const bool ok = P < anw;
             cnt += __popc(__ballot_sync(FULL, ok));
             const uint32_t pos = ok ? ((tail + 4u * lane + k) & (CAP - 1)) : CAP;
-            q.tk[pos] = make_uint2(__float_as_uint(R[k]), (sl << 29) | (al0 + P));
+            q.tk[tk_slot(pos)] = make_uint2(__float_as_uint(R[k]), (sl << 29) | (al0 + P));
         }
         tail += cnt;
         apos = min(apos + total, 0x7fffffffu);
@@ -339,7 +355,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             const uint32_t rank = (uint32_t)__popc(idle & lt);
             if (!act && rank < take) {
                 tk = head + rank;
-                const uint2 t2 = q.tk[tk & (CAP - 1)];
+                const uint2 t2 = q.tk[tk_slot(tk & (CAP - 1))];
                 wl = t2.y & 0x1fffffffu;
                 const TaskRec& m = q.task[t2.y >> 29];
                 const uint4 r0 = *reinterpret_cast<const uint4*>(&m.rr);  // off, degf, ir, -
@@ -416,7 +432,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                     const double dv = __dsub_rn(__dmul_rn(exp_det(x), q.v[pos]), m.K);
                     s1 = __dadd_rn(s1, dv);
                     s2 = __fma_rn(dv, dv, s2);
-                    jsum += q.tk[pos].x;
+                    jsum += q.tk[tk_slot(pos)].x;
                 }
                 xc += nb;
                 rdy -= nb;
