@@ -523,8 +523,13 @@ int launch_t(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const Fast
     // 27 KB smem per block) measured best at 7 blocks: config 5 81.9 -> 77.3
     // ms, config 4 4.97 -> 4.67 s against 6 blocks.
     // Grid = one wave of resident blocks (the kernel strides over tasks).
-    static int nsm = 0, pad = 0;
-    if (!nsm) {
+    // One-time configuration per instantiation (a function-local static, so
+    // concurrent first calls from several host threads initialise it once).
+    struct LaunchCfg {
+        int nsm, pad;
+    };
+    static const LaunchCfg lc = [] {
+        int nsm = 0, pad = 0;
         int dev = 0, smem_sm = 0;
         cudaFuncAttributes fa;
         cudaGetDevice(&dev);
@@ -561,7 +566,9 @@ int launch_t(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const Fast
             fprintf(stderr,
                     "entry_walk_kernel<%d>: %d SMs, occupancy %d blocks/SM, pad %d B, carveout %d%%\n",
                     WPR, nsm, resident, pad, pct);
-    }
+        return LaunchCfg{nsm, pad};
+    }();
+    const int nsm = lc.nsm, pad = lc.pad;
     const uint64_t warps = nrows * WPR;
     const uint64_t blocks = (warps + 3) / 4;
     const uint64_t cap = (uint64_t)nsm * ENTRY_MIN_BLOCKS;
