@@ -521,8 +521,19 @@ def test_config2_hub_rows_match_reference_statistically(pb, ref):
     k3 = pb.entries_estimate(m, cfg.v, rows, p)
     xs = pb.splitting_product(m, cfg.v, p)[rows]
     rm = ref.matrix_from_csr(cfg.csr)
-    rv, rse, _ = rm.entries(cfg.v, rows, cfg.beta, cfg.n_steps, cfg.walkers, 1, 22, workers=1,
-                            threads=os.cpu_count() or 1)
+    # one reference call per row with its own seed (within one call the
+    # reference reuses its walker streams for every entry, so the rows of a
+    # call are correlated samples)
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(k):
+        return rm.entries(cfg.v, rows[k:k + 1], cfg.beta, cfg.n_steps, cfg.walkers, 1,
+                          2000 + k, workers=1, threads=1)
+
+    with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+        res = list(ex.map(one, range(len(rows))))
+    rv = np.array([r[0][0] for r in res])
+    rse = np.array([r[1][0] for r in res])
     z3 = (k3.values - xs) / k3.std_errors
     zr = (rv - xs) / rse
     # same per-row behaviour (mean z within 3 combined standard errors)
@@ -533,6 +544,8 @@ def test_config2_hub_rows_match_reference_statistically(pb, ref):
         assert abs(d.sum() / math.sqrt((s ** 2).sum())) < 4.0
     # direct agreement of the two samplers
     zd = (k3.values - rv) / np.sqrt(k3.std_errors ** 2 + rse ** 2)
+    print(f"config2: z3 mean {z3.mean():.3f} zr mean {zr.mean():.3f} zd mean {zd.mean():.3f} "
+          f"max|zd| {np.abs(zd).max():.2f}")
     assert abs(zd.mean()) < 0.5 and np.sum(np.abs(zd) > 5) <= 2, (zd.mean(), np.abs(zd).max())
 
 
