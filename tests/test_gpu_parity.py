@@ -601,3 +601,43 @@ def test_config5_rows_match_reference_statistically(pb, ref):
     print(f"config5: zd mean {zd.mean():.3f} max|zd| {np.abs(zd).max():.2f} "
           f"jumps {k3.jumps.sum()} vs {rj.sum()} z_jumps {zj:.2f}")
     assert abs(zj) < 4.0, (zj, k3.jumps.sum(), rj.sum())
+
+
+@pytest.mark.parametrize("idx,nrows", [(1, 128), (3, 120), (4, 32)])
+def test_config_rows_match_reference_statistically(pb, ref, idx, nrows):
+    """Full-size configs 1, 3 and 4: K3 against the reference's
+    own entry_estimate (estimator.cpp:169-206), one seed per row, on rows
+    drawn from the config's own row set.  Entry by entry within combined
+    standard errors, both unbiased in aggregate against the splitting
+    product, and the same jump law (config 4 walks ~40 jumps per walker, so
+    this checks the continuous-clock law on long paths)."""
+    cfg = pb.build_config(idx, 1.0)
+    m = pb.split(cfg.csr)
+    pool = cfg.rows if cfg.rows is not None else np.arange(cfg.csr.n)
+    rng = np.random.default_rng(40 + idx)
+    rows = np.sort(rng.choice(pool, nrows, replace=False)).astype(np.uint32)
+    p = pb.PathParams(cfg.beta, cfg.n_steps, cfg.walkers, pb.Splitting.Strang, 41)
+    k3 = pb.entries_estimate(m, cfg.v, rows, p)
+    xs = pb.splitting_product(m, cfg.v, p)[rows]
+    del m
+    rm = ref.matrix_from_csr(cfg.csr)
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(k):
+        return rm.entries(cfg.v, rows[k:k + 1], cfg.beta, cfg.n_steps, cfg.walkers, 1,
+                          3000 + k, workers=1, threads=1)
+
+    with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+        res = list(ex.map(one, range(len(rows))))
+    rv = np.array([r[0][0] for r in res])
+    rse = np.array([r[1][0] for r in res])
+    rj = np.array([r[2][0] for r in res], np.float64)
+    for d, s in ((k3.values - xs, k3.std_errors), (rv - xs, rse)):
+        assert abs(d.sum() / math.sqrt((s ** 2).sum())) < 4.0
+    zd = (k3.values - rv) / np.sqrt(k3.std_errors ** 2 + rse ** 2)
+    dj = k3.jumps.astype(np.float64) - rj
+    zj = dj.sum() / math.sqrt((dj ** 2).sum())
+    print(f"config{idx}: zd mean {zd.mean():.3f} max|zd| {np.abs(zd).max():.2f} "
+          f"jumps {int(k3.jumps.sum())} vs {int(rj.sum())} z_jumps {zj:.2f}")
+    assert abs(zd.mean()) < 0.6 and np.sum(np.abs(zd) > 4) <= 1, (zd.mean(), np.abs(zd).max())
+    assert abs(zj) < 4.0, (zj, k3.jumps.sum(), rj.sum())
