@@ -279,3 +279,26 @@ def _build_cpp_demo(out_dir):
 
 def test_cpp_header_api_compiles_and_links(tmp_path, pb):
     _build_cpp_demo(tmp_path)
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/proj/include"),
+                    reason="reference headers not present (GPU box)")
+def test_integration_binding_compiles_against_reference(tmp_path):
+    """The C++ binding INTEGRATION.md asks a maintainer to add next to
+    proj/include/expmc/estimator.hpp compiles against the reference's own
+    headers and include/expmc_b200.h (syntax and types only)."""
+    import shutil
+    import subprocess
+
+    gxx = shutil.which("g++")
+    if gxx is None:
+        pytest.skip("no g++")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    doc = open(os.path.join(root, "INTEGRATION.md")).read()
+    i = doc.index("// proj/include/expmc/gpu_backend.hpp")
+    src = tmp_path / "gpu_backend.cpp"
+    src.write_text(doc[i:doc.index("```", i)] + "\nint main() { return 0; }\n")
+    r = subprocess.run([gxx, "-std=c++20", "-fsyntax-only", "-Wno-pragma-once-outside-header",
+                        "-I/root/reference/proj/include", "-I" + os.path.join(root, "include"),
+                        str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
