@@ -553,7 +553,8 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
     }
     // W >= 2^29 walkers per entry: the grouped large-W path (K3 packs walker
     // indices into 29 bits)
-    const bool big = fast && p->samples >= (1ull << 29);
+    static const bool force_big = getenv("EXPMC_FORCE_BIG") != nullptr;  // experiments only
+    const bool big = fast && (p->samples >= (1ull << 29) || force_big);
     if (nrows == 0) return;
     DeviceGuard g(h->device);
     cudaStream_t s = h->stream;
