@@ -191,62 +191,101 @@ def traffic_from_profiles(cfg_idx):
 
 
 # ------------------------------------------------------- reference (CPU)
-def cpu_reference_rate(cfg, seed, target_s, steps=1, warmup=0):
-    """The reference's own entry_estimate (oracle/_ref, unmodified sources)
-    on bounded row samples, row-parallel on all host cores: each thread calls
-    entry_estimate(..., workers=1) on its rows (SURVEY §8d, the faster of the
-    two CPU modes).  Returns per-step (seconds, jumps, rows)."""
-    import oracle
+def config_dict(idx, name, n, nnz, entries, walkers, n_steps, beta, gpus):
+    """The workload description both arms print (identical dicts: the
+    driver compares them).  beta is rounded to 10 significant digits so a
+    last-bit difference between the two arms' power iterations (config 2)
+    cannot split them."""
+    big = nnz * 32 + n * 32 > 126e6
+    return {"workload": f"cfg{idx}_{name}", "n": int(n), "nnz": int(nnz),
+            "entries": int(entries), "walkers_per_entry": int(walkers),
+            "n_steps": int(n_steps), "beta": float(f"{beta:.10g}"), "splitting": "strang",
+            "parallelism": f"rows sharded x{gpus}",
+            "l2": "inputs larger than L2 (no flush)" if big else
+                  "inputs L2-resident (no flush; cache-resident config)"}
 
-    ref = oracle.Ref()
+
+def cpu_reference_rate(matrix, v, rows_all, walkers, n_steps, beta, seed, target_s, steps=1,
+                       warmup=0):
+    """The reference's own entry_estimate (oracle/_ref, unmodified sources) on
+    bounded row samples, row-parallel on all host cores: each thread calls
+    entry_estimate(..., workers=1) on its rows (SURVEY §8d, the faster of the
+    two CPU modes).
+
+    Also splits off the reference's O(n) per-call setup (node_factors,
+    proj/src/estimator.cpp:41-45, :177-178, plus the thread pool of
+    parallel_samples, :50-68): the first sample's rows are re-run with
+    samples = 1 on the same threads; that time is the setup the sample paid,
+    and jumps / (time - setup) is the path-only rate.  Returns
+    (per-step [(seconds, jumps, rows)], cores, split dict)."""
     cores = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    rm = ref.matrix_from_csr(cfg.csr)
-    setup_s = time.perf_counter() - t0
-    rows_all = np.arange(cfg.csr.n, dtype=np.uint64) if cfg.rows is None else \
-        cfg.rows.astype(np.uint64)
-    # calibrate: one row per core
     rng = np.random.default_rng(1234)
     cal = rng.choice(rows_all, size=min(cores, len(rows_all)), replace=False)
     t = time.perf_counter()
-    rm.entries(cfg.v, cal, cfg.beta, cfg.n_steps, cfg.walkers, 1, seed, workers=1,
-               threads=cores)
+    matrix.entries(v, cal, beta, n_steps, walkers, 1, seed, workers=1, threads=cores)
     t_cal = max(time.perf_counter() - t, 1e-3)
     per_step = max(len(cal), int(len(cal) * max(1.0, target_s / t_cal)))
     per_step = min(per_step, len(rows_all))
-    out = []
+    out, first = [], None
     for k in range(warmup + steps):
         sample = np.sort(rng.choice(rows_all, size=per_step, replace=False))
+        if first is None:
+            first = sample
         t = time.perf_counter()
-        _, _, j = rm.entries(cfg.v, sample, cfg.beta, cfg.n_steps, cfg.walkers, 1, seed + k,
-                             workers=1, threads=cores)
+        _, _, j = matrix.entries(v, sample, beta, n_steps, walkers, 1, seed + k, workers=1,
+                                 threads=cores)
         dt = time.perf_counter() - t
         if k >= warmup:
             out.append((dt, int(j.sum()), per_step))
-    return out, cores, setup_s
+    t = time.perf_counter()
+    _, _, j1 = matrix.entries(v, first, beta, n_steps, 1, 1, seed, workers=1, threads=cores)
+    setup_s = time.perf_counter() - t
+    s0, j0, r0 = out[0]
+    path_s = max(s0 - setup_s, 1e-9)
+    split = {"setup_per_call_s": setup_s * cores / r0,
+             "setup_share": setup_s / s0,
+             "path_only_value": j0 / path_s,
+             "path_only_entries_per_s": r0 / path_s,
+             "setup_how": f"same {r0} rows re-run with samples=1 (node_factors O(n) + "
+                          f"thread pool per call), row-parallel on {cores} threads"}
+    return out, cores, split
 
 
-def run_reference(args, cfg):
-    steps, cores, setup_s = cpu_reference_rate(cfg, args.seed, args.cpu_seconds,
-                                               steps=args.steps, warmup=args.warmup)
+def run_reference(args):
+    """bench.py --impl reference: the unmodified reference (oracle/_ref) on
+    inputs built by the reference and the oracle only (oracle/inputs.py) —
+    the product library is never loaded in this process."""
+    from oracle import inputs as oi
+
+    t0 = time.perf_counter()
+    rc = oi.build_config(args.config, args.scale)
+    setup_s = time.perf_counter() - t0
+    rows_all = np.arange(rc.n, dtype=np.uint64) if rc.rows is None else \
+        rc.rows.astype(np.uint64)
+    steps, cores, split = cpu_reference_rate(rc.matrix, rc.v, rows_all, rc.walkers, rc.n_steps,
+                                             rc.beta, args.seed, args.cpu_seconds,
+                                             steps=args.steps, warmup=args.warmup)
     secs = sum(s for s, _, _ in steps)
     jumps = sum(j for _, j, _ in steps)
     rows = sum(r for _, _, r in steps)
     value = jumps / secs
-    sample = (f"{steps[0][2]} uniformly sampled rows per step x {cfg.walkers} walkers, "
-              f"N={cfg.n_steps}, row-parallel entry_estimate(workers=1) on {cores} threads")
+    sample = (f"{steps[0][2]} uniformly sampled rows per step (of {rc.nrows}) x {rc.walkers} "
+              f"walkers, N={rc.n_steps}, row-parallel entry_estimate(workers=1) on {cores} "
+              f"threads")
     line = {
         "impl": "reference", "metric": "path transitions/s", "value": value,
         "unit": "transitions/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / len(steps),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "entries_per_s": rows / secs,
-        "config": {"workload": f"cfg{cfg.idx}_{cfg.name}", "n": cfg.csr.n, "nnz": cfg.csr.nnz,
-                   "walkers_per_entry": cfg.walkers, "n_steps": cfg.n_steps, "beta": cfg.beta,
-                   "splitting": "strang", "parallelism": f"{cores} host threads"},
+        "data": "synthetic (seeded generators, SURVEY §8d)", "entries_per_s": rows / secs,
+        "config": config_dict(rc.idx, rc.name, rc.n, rc.nnz, rc.nrows, rc.walkers, rc.n_steps,
+                              rc.beta, args.gpus),
         "cpu_baseline": {"value": value, "unit": "transitions/s", "cores": cores,
-                         "kind": "reference", "sample": sample,
-                         "matrix_setup_s": setup_s},
+                         "kind": "reference", "sample": sample, "rng": "pcg32 (reference)",
+                         "inputs_setup_s": setup_s,
+                         "inputs": "reference generate() (BA) / oracle/inputs_gen.c (FD, WS, "
+                                   "vectors, rows); no product library in this process",
+                         **split},
         "e2e": {"value": value, "unit": "transitions/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -263,16 +302,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        import paper_1904_12759_b200 as pb
-
-        lam = None
-        if args.config == 2:  # beta = 0.5 / lambda_max from the reference's own stats()
-            import oracle
-
-            probe = pb.build_config(2, args.scale, lambda_max=1.0)
-            lam = oracle.Ref().matrix_from_csr(probe.csr).lambda_max(100)
-        cfg = pb.build_config(args.config, args.scale, lambda_max=lam)
-        run_reference(args, cfg)
+        run_reference(args)
         return 0
 
     import torch
@@ -288,7 +318,17 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     t_setup = time.perf_counter()
-    cfg = pb.build_config(args.config, args.scale)
+    if dist:
+        # ranks share one CSR cache: rank 0 generates (BA 1e7 is sequential,
+        # ~8 s), the others load the checksummed file
+        os.environ.setdefault("EXPMC_CSR_CACHE", "/tmp/expmc_csr_cache")
+        if rank == 0:
+            cfg = pb.build_config(args.config, args.scale)
+        dist.barrier()
+        if rank != 0:
+            cfg = pb.build_config(args.config, args.scale)
+    else:
+        cfg = pb.build_config(args.config, args.scale)
     m = pb.split(cfg.csr, device=local)
     rows_all = np.arange(cfg.csr.n, dtype=np.uint32) if cfg.rows is None else cfg.rows
     rows = shard_rows(rows_all, rank, world)
@@ -362,16 +402,7 @@ def main():
 
     # roofline of the walker kernel on this rank (B_alg = 64 J + 48 E)
     j_step_rank = int(jtot.item()) / K
-    balg = 64.0 * j_step_rank + 48.0 * nrows
-    peak, peak_src = peak_hbm()
-    achieved = balg / (kern_ms / 1e3) / 1e9
-    traffic = traffic_from_profiles(cfg.idx) if args.scale == 1.0 else None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                "kernel": "entry_fast_kernel", "kernel_ms": kern_ms,
-                "algorithmic_bytes_per_launch": balg,
-                "bytes_model": "64 B per jump (neighbour-id sector + landing 32-B row record) "
-                               "+ 48 B per entry (start record + value/SE)"}
+    roofline = make_roofline(cfg, j_step_rank, nrows, kern_ms, args.scale)
 
     line = {
         "metric": "path transitions/s", "value": value, "unit": "transitions/s",
@@ -382,42 +413,127 @@ def main():
         "paths_per_s": total_entries * cfg.walkers / secs,
         # segment-steps (N per path) for comparison with PAPER.md:314
         "segment_steps_per_s": total_entries * cfg.walkers * cfg.n_steps / secs,
-        "config": {"workload": f"cfg{cfg.idx}_{cfg.name}", "n": cfg.csr.n, "nnz": cfg.csr.nnz,
-                   "entries": len(rows_all), "walkers_per_entry": cfg.walkers,
-                   "n_steps": cfg.n_steps, "beta": cfg.beta, "splitting": "strang",
-                   "rng": "philox4x32-10", "parallelism": f"rows sharded x{world}",
-                   "l2": "inputs larger than L2 (no flush)" if cfg.csr.nnz * 4 + cfg.csr.n * 32 >
-                   126e6 else "inputs L2-resident (no flush; cache-resident config)",
-                   "setup_s": setup_s},
+        "config": config_dict(cfg.idx, cfg.name, cfg.csr.n, cfg.csr.nnz, len(rows_all),
+                              cfg.walkers, cfg.n_steps, cfg.beta, world),
+        "rng": "philox4x32-10", "setup_s": setup_s,
         "clocks": clk, "gpu_launches": launches, "roofline": roofline,
     }
 
-    if rank == 0 and world == 1 and not args.kernel_only:
-        if not args.no_ceiling:
+    if not args.kernel_only:
+        if rank == 0 and world == 1 and not args.no_ceiling:
             line["gather_ceiling"] = gather_ceiling(pb, m, cfg, rows_d, nrows, j_step_rank,
                                                     stream, sp)
             line["gather_ceiling"]["frac_of_ceiling"] = \
                 (j_step_rank / (kern_ms / 1e3)) / line["gather_ceiling"]["transitions_per_s"]
         if not args.no_e2e:
-            line["e2e"] = e2e(pb, m, cfg, rows, args, K, Wm)
+            line["e2e"] = e2e(pb, m, cfg, rows, args, K, Wm, dist, world, len(rows_all))
         if not args.no_cpu_baseline:
-            try:
-                st, cores, ref_setup = cpu_reference_rate(cfg, args.seed, args.cpu_seconds)
-                s, j, r = st[0]
-                line["cpu_baseline"] = {
-                    "value": j / s, "unit": "transitions/s", "cores": cores,
-                    "kind": "reference",
-                    "sample": f"{r} uniformly sampled rows x {cfg.walkers} walkers, "
-                              f"row-parallel entry_estimate(workers=1), {s:.1f} s",
-                    "entries_per_s": r / s, "matrix_setup_s": ref_setup}
-            except Exception as e:  # reference library missing on this box
-                line["cpu_baseline"] = {"value": None, "unit": "transitions/s", "cores": 0,
-                                        "kind": "reference", "sample": f"unavailable: {e}"}
+            if rank == 0:
+                line["cpu_baseline"] = cpu_baseline_leg(cfg, rows_all, args)
+            if dist:
+                dist.barrier()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def cpu_baseline_leg(cfg, rows_all, args):
+    """The reference's entry_estimate on this box's host cores (rank 0 only),
+    on a bounded row sample of the same workload."""
+    try:
+        import oracle
+
+        t0 = time.perf_counter()
+        rm = oracle.Ref().matrix_from_csr(cfg.csr)
+        ref_setup = time.perf_counter() - t0
+        st, cores, split = cpu_reference_rate(rm, cfg.v, rows_all.astype(np.uint64),
+                                              cfg.walkers, cfg.n_steps, cfg.beta, args.seed,
+                                              args.cpu_seconds)
+        s, j, r = st[0]
+        return {"value": j / s, "unit": "transitions/s", "cores": cores, "kind": "reference",
+                "sample": f"{r} uniformly sampled rows x {cfg.walkers} walkers, "
+                          f"row-parallel entry_estimate(workers=1), {s:.1f} s",
+                "entries_per_s": r / s, "matrix_setup_s": ref_setup, **split}
+    except Exception as e:  # reference library missing on this box
+        return {"value": None, "unit": "transitions/s", "cores": 0, "kind": "reference",
+                "sample": f"unavailable: {e}"}
+
+
+def source_sha():
+    """Hash of the kernel sources: ties an ncu capture to the code it measured."""
+    import hashlib
+
+    h = hashlib.sha256()
+    d = os.path.join(ROOT, "paper_1904_12759_b200", "csrc")
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cu", ".cuh", ".cpp", ".h")):
+            h.update(f.encode())
+            with open(os.path.join(d, f), "rb") as fh:
+                h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def _load_json(*parts):
+    try:
+        with open(os.path.join(ROOT, *parts)) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def make_roofline(cfg, jumps, entries, kern_ms, scale):
+    """Roofline of the walker kernel (K3) for one launch.
+
+    * achieved / frac: SURVEY §8d's algorithmic bytes, 64 B per jump
+      (neighbour-id sector + landing row record) + 48 B per entry, over the
+      kernel's CUDA-event time.  Config 5's walked set (5 GB) is HBM-bound:
+      peak = measured copy bandwidth.  Configs 1-4 are served from L2 (93%+
+      hits on config 4, everything on 1-3): peak = the measured L2
+      random-gather ceiling (K6 on an L2-resident table, profiles/r02/
+      l2_gather_peak.json), counted with the same 64 B per jump.
+    * frac_design_bytes: the bytes this design actually has to move (one
+      32-B fat Edge sector per jump + 48 B per entry) against HBM.
+    * traffic / frac_dram_measured / sector_efficiency: from the committed
+      ncu --set full capture of this config (profiles/r02/ncu_cfg<i>.json),
+      with the source hash it was taken at (traffic_same_source)."""
+    hbm, hbm_src = peak_hbm()
+    secs = kern_ms / 1e3
+    balg = 64.0 * jumps + 48.0 * entries
+    bdes = 32.0 * jumps + 48.0 * entries
+    l2 = _load_json("profiles", "r02", "l2_gather_peak.json")
+    if cfg.idx == 5 or l2 is None:
+        bound, peak, src = "hbm", hbm, hbm_src
+    else:
+        bound, peak = "l2", float(l2["gbs_model_64B"])
+        src = f"measured L2 random-gather ceiling ({l2['how']})"
+    achieved = balg / secs / 1e9
+    r = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
+         "frac": achieved / peak, "peak_source": src, "kernel": "entry_walk_kernel",
+         "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": balg,
+         "bytes_model": "64 B per jump (neighbour-id sector + landing 32-B row record) "
+                        "+ 48 B per entry (start record + value/SE)",
+         "design_bytes_per_launch": bdes,
+         "frac_design_bytes": bdes / secs / 1e9 / hbm,
+         "traffic": None}
+    prof = _load_json("profiles", "r02", f"ncu_cfg{cfg.idx}.json") if scale == 1.0 else None
+    if prof:
+        tr = float(prof["dram_bytes_per_launch"])
+        r["traffic"] = tr
+        r["frac_dram_measured"] = tr / secs / 1e9 / hbm
+        r["traffic_capture"] = prof.get("capture")
+        r["traffic_same_source"] = prof.get("source_sha") == source_sha()
+        sec = prof.get("l1tex_ld_sectors_per_launch")
+        if sec:
+            r["sector_efficiency"] = (32.0 * jumps + 40.0 * entries) / (32.0 * float(sec))
+            r["sector_efficiency_def"] = ("useful load bytes (32 B Edge per jump + 32 B start "
+                                          "record + 8 B rate per entry) / (l1tex global-load "
+                                          "sectors x 32)")
+        for k in ("l2_hit_rate", "l1_hit_rate", "issue_active", "warp_instructions"):
+            if k in prof:
+                r["ncu_" + k] = prof[k]
+    return r
 
 
 def gather_ceiling(pb, m, cfg, rows_d, nrows, j_step, stream, sp):
@@ -445,10 +561,12 @@ def gather_ceiling(pb, m, cfg, rows_d, nrows, j_step, stream, sp):
             "chains_per_row": chains, "chain_len": length, "ms": t * 1e3}
 
 
-def e2e(pb, m, cfg, rows, args, K, Wm):
+def e2e(pb, m, cfg, rows, args, K, Wm, dist, world, nrows_all):
     """Same metric through the public host API (C ABI entries call) with
     pinned host buffers: H2D of v (+ rows) and D2H of value/SE/jumps inside
-    the timed region."""
+    the timed region.  At N > 1 every rank calls it on its row shard (each
+    rank writes its slice into its own pinned host buffers); the step time is
+    the max over ranks, bracketed by barriers."""
     import torch
 
     n, nrows = cfg.csr.n, len(rows)
@@ -469,15 +587,27 @@ def e2e(pb, m, cfg, rows, args, K, Wm):
     for k in range(Wm):
         call(k)
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     t = time.perf_counter()
     jumps = 0
     for k in range(K):
         jumps += call(k)
     secs = time.perf_counter() - t
+    if dist:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        tt = torch.tensor([secs, float(jumps)], dtype=torch.float64, device=dev)
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt)
+        secs, jumps = float(mx[0].item()), int(tt[1].item())
+    h2d = world * n * 8 + (0 if full else nrows_all * 4)
     return {"value": jumps / secs, "unit": "transitions/s",
-            "h2d_bytes_per_step": n * 8 + (0 if full else nrows * 4),
-            "d2h_bytes_per_step": nrows * 24, "entries_per_s": nrows * K / secs,
-            "ms_per_step": 1e3 * secs / K, "api": "expmc_cuda_entries (host buffers, pinned)"}
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": nrows_all * 24,
+            "entries_per_s": nrows_all * K / secs, "ms_per_step": 1e3 * secs / K,
+            "api": "expmc_cuda_entries (host buffers, pinned)" +
+                   (f"; one call per rank on its row shard, max over {world} ranks"
+                    if world > 1 else "")}
 
 
 if __name__ == "__main__":

@@ -254,16 +254,48 @@ def test_vector_and_tc_shards_combine_in_rank_order_gloo(world):
     assert te == wt
 
 
-def test_bench_reference_arm_cpu(ref):
-    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                          "--config", "1", "--scale", "0.05", "--steps", "1", "--warmup", "0",
-                          "--cpu-seconds", "0.5"], capture_output=True, text=True, timeout=300)
+_REF_ARM_CHILD = r"""
+import json, runpy, sys
+sys.argv = ["bench.py"] + sys.argv[1:]
+try:
+    runpy.run_path(%r, run_name="__main__")
+except SystemExit as e:
+    assert not e.code, e.code
+maps = open("/proc/self/maps").read()
+print(json.dumps({"maps_product": "libexpmc_b200" in maps, "maps_ref": "libexpmc_ref" in maps,
+                  "product_imported": "paper_1904_12759_b200" in sys.modules}))
+"""
+
+
+@pytest.mark.parametrize("cfg,scale", [(1, 0.05), (2, 0.02), (4, 0.0005)])
+def test_bench_reference_arm_cpu(ref, pb, cfg, scale):
+    """--impl reference runs the reference without the product library in
+    its process, and prints the same config dict as the GPU arm."""
+    code = _REF_ARM_CHILD % os.path.join(ROOT, "bench.py")
+    out = subprocess.run([sys.executable, "-c", code, "--impl", "reference",
+                          "--config", str(cfg), "--scale", str(scale), "--steps", "1",
+                          "--warmup", "0", "--cpu-seconds", "0.3"], capture_output=True,
+                         text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr
-    line = json.loads(out.stdout.strip().splitlines()[-1])
+    lines = [json.loads(x) for x in out.stdout.strip().splitlines() if x.startswith("{")]
+    line, maps = lines[-2], lines[-1]
+    assert maps == {"maps_product": False, "maps_ref": True, "product_imported": False}
     assert line["impl"] == "reference" and line["value"] > 0
     for k in ("metric", "unit", "cpu_baseline", "e2e", "config", "higher_is_better"):
         assert k in line
-    assert line["cpu_baseline"]["kind"] == "reference"
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "reference" and cb["path_only_value"] >= line["value"] * 0.999
+    assert 0.0 <= cb["setup_share"] <= 1.0 and cb["setup_per_call_s"] > 0
+    sys.path.insert(0, ROOT)
+    import bench
+
+    c = pb.build_config(cfg, scale, lambda_max=(ref.generate(1, max(1000, int(1e5 * scale)), m0=5,
+                                                             seed=1).lambda_max(100)
+                                                if cfg == 2 else None))
+    rows = c.csr.n if c.rows is None else len(c.rows)
+    want = bench.config_dict(c.idx, c.name, c.csr.n, c.csr.nnz, rows, c.walkers, c.n_steps,
+                             c.beta, 1)
+    assert line["config"] == want
 
 
 def _build_cpp_demo(out_dir):
