@@ -49,11 +49,13 @@ void fm_philox(const uint32_t ctr[4], uint32_t k0, uint32_t k1, uint32_t out[4])
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
+/* neg_ln_u of csrc/common.cuh: -ln(u), u = (w | 1) 2^-32, same operations
+ * in the same order. */
 float fm_neg_ln_u(uint32_t w) {
-    const float u = ((float)(w >> 9) + 0.5f) * 0x1.0p-23f;
+    const float fx = (float)(w | 1u); /* round to nearest, as __uint2float_rn */
     uint32_t bits;
-    memcpy(&bits, &u, 4);
-    int e = (int)((bits >> 23) & 0xffu) - 127;
+    memcpy(&bits, &fx, 4);
+    int e = (int)(bits >> 23) - 127;
     const uint32_t mb = (bits & 0x007fffffu) | 0x3f800000u;
     float m;
     memcpy(&m, &mb, 4);
@@ -71,8 +73,8 @@ float fm_neg_ln_u(uint32_t w) {
     q = fmaf(q, f, 0.3333418369293213f);
     q = fmaf(q, f, -0.49999988079071045f);
     q = fmaf(q, f, 1.0f);
-    const float ln_u = fmaf((float)e, 0.693147182f, f * q);
-    return -ln_u;
+    const float E = fmaf((float)(32 - e), 0.693147182f, -(f * q));
+    return E > 0.0f ? E : 0.0f;
 }
 
 /* exp_det of csrc/common.cuh: the kernel's deterministic fp64 exp

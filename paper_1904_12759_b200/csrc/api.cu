@@ -229,12 +229,19 @@ void finish_split(expmc_matrix* h) {
     launch_split_pack(n, m.row_offset, m.weight, m.diag, m.d, m.rate, m.cum, m.uniform_row, m.rec,
                       sc + 1, reinterpret_cast<unsigned int*>(sc + 2), s);
     after_launch(n ? 1 : 0);
+    launch_rate_sum(n, m.rate, reinterpret_cast<double*>(sc + 3), s);
+    after_launch(n ? 1 : 0);
     unsigned long long res[4];
     CK(cudaMemcpyAsync(res, sc, sizeof(res), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     m.dmax = res[1];
     m.any_nonuniform = (res[2] & 0xffffffffull) != 0;
     m.dbar = n > 0 ? (double)nnz / (double)n : 0.0;  // sparse_matrix.cpp:138-141
+    {
+        double rs;
+        std::memcpy(&rs, &res[3], 8);
+        m.mean_rate = n > 0 ? rs / (double)n : 0.0;
+    }
     if (m.any_nonuniform) {
         m.alias_thr = h->alloc<uint32_t>(nnz);
         m.alias_idx = h->alloc<uint32_t>(nnz);

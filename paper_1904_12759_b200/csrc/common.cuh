@@ -133,15 +133,22 @@ __device__ __forceinline__ U4 philox4x32_10(U4 c, const PhiloxKeys& K) {
 constexpr uint32_t kTagEntry = 0x454e5452u;  // 'ENTR'
 constexpr uint32_t kTagScatter = 0x56454354u; // 'VECT' (vector / tc)
 
-// -ln(u) for u = ((w >> 9) + 0.5) * 2^-23 in (0, 1), fp32, using only
-// IEEE-exact operations (mul, sub, fma) so the CPU model in
-// oracle/fast_model.c reproduces it bit for bit.  u = 2^e m with
-// m in [sqrt(1/2), sqrt(2)); ln(m) = f q(f), f = m - 1 (exact), q a degree-8
-// Chebyshev fit of log1p(f)/f on [sqrt(1/2)-1, sqrt(2)-1] (rel. err 2.7e-8).
+// -ln(u) ~ Exp(1) from one 32-bit Philox word, fp32, IEEE-exact operations
+// only (so oracle/fast_model.c fm_neg_ln_u reproduces it bit for bit).
+// u = x 2^-32 with x = w | 1: the midpoint of one of 2^31 equal bins of
+// (0, 1), so P(E > y) matches e^-y to within 2^-31 everywhere, up to the
+// largest draw 32 ln 2 = 22.18 (the reference draws a 53-bit uniform,
+// rng.hpp:47-49, sampler.cpp:10-16; tests/test_gpu_rng_law.py bounds the
+// difference).  x = 2^e m exactly up to fp32 rounding of x (24 bits); with
+// m folded into [sqrt(1/2), sqrt(2)), -ln u = (32 - e) ln 2 - ln m, ln m =
+// f q(f), f = m - 1 (exact), q a degree-8 Chebyshev fit of log1p(f)/f (rel.
+// err 2.7e-8).  Near u = 1 (e = 32) the ln 2 term vanishes exactly.
+// Absolute error <= 1.5e-7 max(1, E).  (A 64-entry table variant with a
+// degree-3 log1p measured 1.2 ms slower on config 5: the L1 lookups compete
+// with the gathers, profiles/r02/README.md.)
 __device__ __forceinline__ float neg_ln_u(uint32_t w) {
-    const float u = __fmul_rn(__uint2float_rn(w >> 9) + 0.5f, 0x1.0p-23f);
-    const uint32_t bits = __float_as_uint(u);
-    int e = (int)((bits >> 23) & 0xffu) - 127;
+    const uint32_t bits = __float_as_uint(__uint2float_rn(w | 1u));
+    int e = (int)(bits >> 23) - 127;
     float m = __uint_as_float((bits & 0x007fffffu) | 0x3f800000u);  // [1,2)
     if (m > 1.41421356f) {
         m = __fmul_rn(m, 0.5f);
@@ -157,8 +164,8 @@ __device__ __forceinline__ float neg_ln_u(uint32_t w) {
     q = __fmaf_rn(q, f, 0.3333418369293213f);
     q = __fmaf_rn(q, f, -0.49999988079071045f);
     q = __fmaf_rn(q, f, 1.0f);
-    const float ln_u = __fmaf_rn((float)e, 0.693147182f, __fmul_rn(f, q));
-    return -ln_u;
+    const float E = __fmaf_rn(__int2float_rn(32 - e), 0.693147182f, -__fmul_rn(f, q));
+    return E > 0.0f ? E : 0.0f;
 }
 
 // e^x in fp64 from IEEE-exact operations only (rint, fma, mul, add), so the
@@ -208,7 +215,11 @@ __device__ const double2 kExpTab[32] = {
 __device__ __forceinline__ double exp_det(double x) {
     x = x > 710.0 ? 710.0 : x;
     x = x < -746.0 ? -746.0 : x;
-    const double n = rint(__dmul_rn(x, 0x1.71547652b82fep+5));  // 32 / ln2
+    // n = rint(x 32/ln2) by the 1.5 2^52 shifter (round-to-nearest-even, as
+    // rint; |x 32/ln2| < 2^15): the integer sits in the low word, no
+    // FRND / F2I on the slow pipes
+    const double sh = __dadd_rn(__dmul_rn(x, 0x1.71547652b82fep+5), 0x1.8p52);  // 32 / ln2
+    const double n = __dsub_rn(sh, 0x1.8p52);
     double r = __fma_rn(-n, 0x1.62e42fee00000p-6, x);  // ln2/32, hi part (exact n*hi)
     r = __fma_rn(-n, 0x1.a39ef35793c76p-38, r);         // ln2/32, lo part
     double p = 1.0 / 720.0;
@@ -218,7 +229,7 @@ __device__ __forceinline__ double exp_det(double x) {
     p = __fma_rn(p, r, 0.5);
     p = __fma_rn(p, r, 1.0);
     p = __dmul_rn(p, r);  // e^r - 1
-    const int ni = __double2int_rn(n);
+    const int ni = (int)__double2loint(sh);
     const double2 t = __ldg(&kExpTab[ni & 31]);
     const double y = __dadd_rn(t.x, __fma_rn(t.x, p, t.y));
     const int k = ni >> 5;

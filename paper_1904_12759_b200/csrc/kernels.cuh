@@ -24,6 +24,7 @@ struct DevSplit {
     double dbar = 0.0;
     uint64_t dmax = 0;
     bool any_nonuniform = false;
+    double mean_rate = 0.0;      // launch heuristics only (K3 occupancy choice)
     // walk layout
     RowRec* rec = nullptr;       // n packed 32-B row records
     uint32_t* alias_thr = nullptr; // nnz (only if any_nonuniform)
@@ -56,6 +57,7 @@ void launch_split_pack(uint64_t n, const uint64_t* row_ptr, const double* weight
                        const double* diag, double* d, double* rate, double* cum,
                        uint8_t* uniform_row, RowRec* rec, unsigned long long* dmax,
                        unsigned int* any_nonuniform, cudaStream_t s);
+void launch_rate_sum(uint64_t n, const double* rate, double* out, cudaStream_t s);
 void launch_alias_build(uint64_t n, const uint64_t* row_ptr, const double* weight,
                         const double* rate, const uint8_t* uniform_row, uint32_t* thr,
                         uint32_t* alias, double* p, uint32_t* small, uint32_t* large,

@@ -220,6 +220,24 @@ void launch_split_pack(uint64_t n, const uint64_t* row_ptr, const double* weight
         n, row_ptr, weight, diag, d, rate, cum, uniform_row, rec, dmax, any_nonuniform);
 }
 
+// Sum of the row rates (launch heuristics only: per-warp atomics, so the
+// last bits depend on the schedule; never feeds a result).
+__global__ void rate_sum_kernel(uint64_t n, const double* __restrict__ rate,
+                                double* __restrict__ out) {
+    double acc = 0.0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        acc += rate[i];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
+void launch_rate_sum(uint64_t n, const double* rate, double* out, cudaStream_t s) {
+    if (n == 0) return;
+    const uint64_t want = (n + 255) / 256;
+    rate_sum_kernel<<<(unsigned)(want < 1184 ? want : 1184), 256, 0, s>>>(n, rate, out);
+}
+
 void launch_alias_build(uint64_t n, const uint64_t* row_ptr, const double* weight,
                         const double* rate, const uint8_t* uniform_row, uint32_t* thr,
                         uint32_t* alias, double* p, uint32_t* small, uint32_t* large,

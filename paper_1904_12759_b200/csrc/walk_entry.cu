@@ -51,8 +51,8 @@ namespace {
 constexpr int kRound = 128;  // gaps per warp round (4 per lane): at most kRound tickets
 constexpr unsigned FULL = 0xffffffffu;
 
-#ifndef ENTRY_MIN_BLOCKS
-#define ENTRY_MIN_BLOCKS 7
+#ifndef ENTRY_SHORT_WALK
+#define ENTRY_SHORT_WALK 8.0 // mean jumps per walker below which 8 blocks/SM run (else 7)
 #endif
 #ifndef ENTRY_TASKS
 #define ENTRY_TASKS 8   // tasks in flight per warp (power of 2, <= 8: slot in 3 ticket bits)
@@ -61,13 +61,16 @@ constexpr unsigned FULL = 0xffffffffu;
 #define ENTRY_CAP 256   // jumper tickets in flight per warp (power of 2, >= 128)
 #endif
 #ifndef ENTRY_CARVE
-#define ENTRY_CARVE 1     // size the smem carveout for ENTRY_MIN_BLOCKS (max L1)
+#define ENTRY_CARVE 1     // size the smem carveout for the resident block count (max L1)
 #endif
 #ifndef ENTRY_DYNAMIC
 #define ENTRY_DYNAMIC 1 // tasks after the first grid-full from a global counter (0: static stride)
 #endif
 #ifndef ENTRY_SWZ
 #define ENTRY_SWZ 0 // 1: swizzle the ticket ring (measured 1.5% slower: the conflicts are not the limiter)
+#endif
+#ifndef ENTRY_UNCOND_LD
+#define ENTRY_UNCOND_LD 1 // issue the jump gather for every lane (no predicated moves behind it)
 #endif
 #ifndef ENTRY_POP_MIN
 #define ENTRY_POP_MIN 2 // run the scheduler once this many lanes are idle
@@ -131,8 +134,8 @@ struct WarpState {
 // tasks remain (ring capacity) [4] jumping lanes [5] active lanes
 #endif
 
-template <int WPR>
-__global__ void __launch_bounds__(128, ENTRY_MIN_BLOCKS)
+template <int WPR, int BL>
+__global__ void __launch_bounds__(128, BL)
 entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rate,
                   const Edge* __restrict__ adj, const uint32_t* __restrict__ thr,
                   const uint32_t* __restrict__ alias, const uint32_t* __restrict__ rows,
@@ -392,13 +395,25 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             }
         }
 #endif
-        // ---- C: one jump for every walker whose sojourn did not end the path
+        // ---- C: one jump for every walker whose sojourn did not end the path.
+        // After the pop every walker still in flight must jump (jmp == act),
+        // so the gather is issued unconditionally (idle lanes re-read slot 0
+        // and are re-initialised at their next pop): the 256-bit load then
+        // lands straight in the loop-carried registers, with no predicated
+        // register moves right behind it to stall on, and its latency hides
+        // behind the accumulation / admission work below until the next
+        // iteration's sojourn reads the new state.
+#if ENTRY_UNCOND_LD
+        {
+#else
         if (jmp) {
+#endif
             const U4 B = philox4x32_10(U4{jc, wl, wi, kTagEntry}, p.rk);
             const uint32_t off = OFF, degf = DEGF;
             uint32_t k = pick_index(B.y, B.w, degf & kDegMask);
-            if ((degf & kNonUniform) && B.z >= __ldg(thr + off + k)) k = __ldg(alias + off + k);
-            ld256(adj + off + k, ea, eb, ec, ed);
+            if (jmp && (degf & kNonUniform) && B.z >= __ldg(thr + off + k))
+                k = __ldg(alias + off + k);
+            ld256(adj + (jmp ? off + k : 0u), ea, eb, ec, ed);
             ew = B.x;
             ++jc;
         }
@@ -408,10 +423,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         // walking (or the first not popped) bounds them.
         const uint32_t minoff = __reduce_min_sync(FULL, act ? tk - xc : ~0u);
         uint32_t rdy = head - xc < minoff ? head - xc : minoff;
-        if (rdy < 32u && !(ocl && rdy >= oend - xc)) {
-            if (tf == tw && !aopen && atask >= ntask) break;  // every task finalized
-            continue;
-        }
+        if (rdy >= 32u || (ocl && rdy >= oend - xc)) {
         __syncwarp();
         while (tf != tw) {
             const TaskRec& m = q.task[tf & (RT - 1)];
@@ -470,6 +482,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 oend = e.x;
             }
         }
+        }
         if (tf == tw && !aopen && atask >= ntask) break;  // every task finalized
     }
 }
@@ -511,23 +524,20 @@ __global__ void combine_parts_kernel(const double4* __restrict__ partial, uint64
     out_jumps[r] = js;
 }
 
-template <int WPR>
-int launch_t(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const FastParams& p,
-             double* value, double* se, uint64_t* jumps, double4* partial, cudaStream_t s) {
-    // Exactly ENTRY_MIN_BLOCKS resident blocks per SM with the smallest
-    // shared-memory carveout that holds them, so the rest of the SM's 256 KB
-    // is L1 for the edge gathers, and no more: padding each block with
-    // dynamic shared memory so that an extra block cannot fit pins the block
-    // count (when the driver sized the carveout for a register-limited
-    // occupancy above the target, config 4 ran 1.8x slower).  v10 (72 regs,
-    // 27 KB smem per block) measured best at 7 blocks: config 5 81.9 -> 77.3
-    // ms, config 4 4.97 -> 4.67 s against 6 blocks.
-    // Grid = one wave of resident blocks (the kernel strides over tasks).
-    // One-time configuration per instantiation (a function-local static, so
-    // concurrent first calls from several host threads initialise it once).
-    struct LaunchCfg {
-        int nsm, pad;
-    };
+// Exactly BL resident blocks per SM with the smallest shared-memory carveout
+// that holds them, so the rest of the SM's 256 KB is L1 for the edge
+// gathers, and no more: padding each block with dynamic shared memory so
+// that an extra block cannot fit pins the block count (when the driver
+// sized the carveout for a register-limited occupancy above the target,
+// config 4 ran 1.8x slower).  One-time configuration per instantiation (a
+// function-local static, so concurrent first calls from several host
+// threads initialise it once).
+struct LaunchCfg {
+    int nsm, pad;
+};
+
+template <int WPR, int BL>
+const LaunchCfg& launch_cfg() {
     static const LaunchCfg lc = [] {
         int nsm = 0, pad = 0;
         int dev = 0, smem_sm = 0;
@@ -536,52 +546,82 @@ int launch_t(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const Fast
         if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
             nsm = 148;
         int pct = -1;
-        if (ENTRY_CARVE && cudaFuncGetAttributes(&fa, entry_walk_kernel<WPR>) == cudaSuccess &&
+        if (ENTRY_CARVE && cudaFuncGetAttributes(&fa, entry_walk_kernel<WPR, BL>) == cudaSuccess &&
             cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) ==
                 cudaSuccess &&
             smem_sm > 0) {
-            constexpr int B = ENTRY_MIN_BLOCKS, kReserve = 1024;
+            constexpr int kReserve = 1024;
             const long st = (long)fa.sharedSizeBytes;
             const int kb[] = {0, 8, 16, 32, 64, 100, 132, 164, 196, 228};
             long cap = smem_sm;
             for (int c : kb)
-                if (c * 1024L >= B * (st + kReserve) && c * 1024L <= smem_sm) {
+                if (c * 1024L >= BL * (st + kReserve) && c * 1024L <= smem_sm) {
                     cap = c * 1024L;
                     break;
                 }
-            const long tmin = smem_sm / (B + 1) - kReserve + 1;  // B+1 blocks must not fit
-            const long tmax = cap / B - kReserve;                 // B blocks must fit in cap
+            const long tmin = smem_sm / (BL + 1) - kReserve + 1;  // BL+1 blocks must not fit
+            const long tmax = cap / BL - kReserve;                 // BL blocks must fit in cap
             if (tmin <= tmax) pad = (int)(tmin > st ? tmin - st : 0);
-            if (pad) cudaFuncSetAttribute(entry_walk_kernel<WPR>,
+            if (pad) cudaFuncSetAttribute(entry_walk_kernel<WPR, BL>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
             // the driver rounds the percentage UP to a supported capacity
             pct = (int)floor(100.0 * cap / smem_sm);
-            cudaFuncSetAttribute(entry_walk_kernel<WPR>,
+            cudaFuncSetAttribute(entry_walk_kernel<WPR, BL>,
                                  cudaFuncAttributePreferredSharedMemoryCarveout, pct);
         }
         int resident = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, entry_walk_kernel<WPR>, 128, pad);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, entry_walk_kernel<WPR, BL>, 128,
+                                                      pad);
         cudaGetLastError();
         if (getenv("EXPMC_DEBUG"))
             fprintf(stderr,
-                    "entry_walk_kernel<%d>: %d SMs, occupancy %d blocks/SM, pad %d B, carveout %d%%\n",
-                    WPR, nsm, resident, pad, pct);
+                    "entry_walk_kernel<%d,%d>: %d SMs, occupancy %d blocks/SM, pad %d B, "
+                    "carveout %d%%\n",
+                    WPR, BL, nsm, resident, pad, pct);
         return LaunchCfg{nsm, pad};
     }();
+    return lc;
+}
+
+template <int WPR, int BL>
+int launch_t(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const FastParams& p,
+             double* value, double* se, uint64_t* jumps, double4* partial, cudaStream_t s) {
+    // Grid = one wave of resident blocks (the kernel strides over tasks).
+    const LaunchCfg& lc = launch_cfg<WPR, BL>();
     const int nsm = lc.nsm, pad = lc.pad;
     const uint64_t warps = nrows * WPR;
     const uint64_t blocks = (warps + 3) / 4;
-    const uint64_t cap = (uint64_t)nsm * ENTRY_MIN_BLOCKS;
+    const uint64_t cap = (uint64_t)nsm * BL;
     const unsigned grid = (unsigned)(blocks < cap ? blocks : cap);
     unsigned int* ctr = reinterpret_cast<unsigned int*>(partial + warps);
 #if ENTRY_DYNAMIC
     cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s);
 #endif
-    entry_walk_kernel<WPR><<<grid, 128, pad, s>>>(m.rec, m.rate, m.adj, m.alias_thr, m.alias_idx,
-                                                rows, nrows, p, partial, ctr);
+    entry_walk_kernel<WPR, BL><<<grid, 128, pad, s>>>(m.rec, m.rate, m.adj, m.alias_thr,
+                                                    m.alias_idx, rows, nrows, p, partial, ctr);
     combine_parts_kernel<WPR><<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(
         partial, nrows, p.W, value, se, jumps);
     return 2;
+}
+
+// Two launch shapes, chosen by the mean walk length (jumps of a walker
+// started at a random row); neither changes a result bit.
+//  * short walks (< ENTRY_SHORT_WALK jumps): 8 resident blocks per SM (32
+//    warps, ~38 KB of L1 left) — the kernel is issue/latency-bound on
+//    scheduling and arithmetic (config 5: 48.9 ms vs 51.1 ms at 7 blocks);
+//  * long walks: 7 blocks (28 warps, ~60 KB of L1 for the outstanding misses
+//    of the dependent gather chains; config 4: 2.95 s vs 4.59 s at 8).
+// Measured, profiles/r02/README.md.  (A Philox / Exp(1) lookahead for long
+// walks, off the gather-to-gather path, measured slower on config 4:
+// 3.25 s.)
+template <int WPR>
+int launch_w(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const FastParams& p,
+             double* value, double* se, uint64_t* jumps, double4* partial, cudaStream_t s) {
+    const double walk = p.beta * m.mean_rate;
+    bool shortw = walk < ENTRY_SHORT_WALK;
+    if (const char* e = getenv("EXPMC_ENTRY_SHAPE")) shortw = atoi(e) == 0;  // A/B only
+    return shortw ? launch_t<WPR, 8>(m, rows, nrows, p, value, se, jumps, partial, s)
+                  : launch_t<WPR, 7>(m, rows, nrows, p, value, se, jumps, partial, s);
 }
 
 }  // namespace
@@ -613,9 +653,9 @@ int launch_entry_fast(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
 #endif
     int k;
     switch (entry_fast_wpr(p.W)) {
-        case 4: k = launch_t<4>(m, rows, nrows, p, value, se, jumps, part, s); break;
-        case 2: k = launch_t<2>(m, rows, nrows, p, value, se, jumps, part, s); break;
-        default: k = launch_t<1>(m, rows, nrows, p, value, se, jumps, part, s); break;
+        case 4: k = launch_w<4>(m, rows, nrows, p, value, se, jumps, part, s); break;
+        case 2: k = launch_w<2>(m, rows, nrows, p, value, se, jumps, part, s); break;
+        default: k = launch_w<1>(m, rows, nrows, p, value, se, jumps, part, s); break;
     }
 #ifdef ENTRY_STATS
 #undef p

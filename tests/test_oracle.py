@@ -148,13 +148,18 @@ def test_model_philox_matches_curand(orc):
 
 
 def test_model_neg_ln_accuracy(orc):
-    ws = np.random.default_rng(0).integers(0, 2**32, 20000, dtype=np.uint64)
-    for w in list(ws) + [0, 511, 512, 2**31, 2**32 - 1]:
+    """neg_ln_u(w) = -ln(u), u = (w | 1) 2^-32 (31-bit midpoint uniform), to
+    1.5e-7 max(1, E) absolute (fp32: x is rounded to 24 bits); never negative."""
+    ws = np.random.default_rng(0).integers(0, 2**32, 40000, dtype=np.uint64)
+    edge = [0, 1, 2, 3, 511, 512, 2**24 - 1, 2**24, 2**24 + 1, 2**31, 2**32 - 129, 2**32 - 128,
+            2**32 - 2, 2**32 - 1]
+    for w in list(ws) + edge:
         w = int(w)
-        u = ((w >> 9) + 0.5) * 2.0 ** -23
-        want = -math.log(u)
+        want = 32 * math.log(2.0) - math.log(w | 1)
         got = orc.neg_ln_u(w)
-        assert abs(got - want) <= 2e-7 * max(1.0, want), (w, got, want)
+        assert got >= 0.0
+        assert abs(got - want) <= 1.5e-7 * max(1.0, want), (w, got, want)
+    assert orc.neg_ln_u(0) == pytest.approx(32 * math.log(2.0), rel=1e-7)
 
 
 def test_model_exp_det_accuracy(orc):
