@@ -121,6 +121,27 @@ int expmc_cuda_entry_estimate(expmc_matrix* m, const double* v, uint64_t nv, uin
 int expmc_cuda_entries(expmc_matrix* m, const double* v, uint64_t nv, const uint32_t* rows,
                        uint64_t nrows, const expmc_path_params* p, double* value,
                        double* std_error, uint64_t* jumps, uint64_t* total_jumps);
+/* The batched entry estimator over several replicas of one matrix (the
+ * reference's `workers` knob, estimator.hpp:59-61 / estimator.cpp:50-68,
+ * mapped to devices): rows split into nh contiguous equal shards, shard k
+ * on handles[k] (one per GPU, or several on one GPU), all driven
+ * concurrently; each shard's slice lands directly in value / std_error /
+ * jumps.  Bitwise identical to expmc_cuda_entries on one handle for any nh. */
+int expmc_cuda_entries_multi(expmc_matrix* const* handles, int nh, const double* v, uint64_t nv,
+                             const uint32_t* rows, uint64_t nrows, const expmc_path_params* p,
+                             double* value, double* std_error, uint64_t* jumps,
+                             uint64_t* total_jumps);
+/* Staged-v reuse for repeated host entry calls with the same v (the
+ * reference passes v on every call, estimator.hpp:59-60, and recomputes its
+ * O(n) node factors each time, estimator.cpp:177-178).  With the cache
+ * enabled, a call whose v pointer and length equal the last staged ones
+ * skips the H2D copy, the finiteness scan and the repack of v into the
+ * walk layout; the caller must call expmc_cuda_invalidate_v after changing
+ * v in place.  Off by default (every call stages v).  v_stagings counts the
+ * stagings performed (measurement / tests). */
+int expmc_cuda_set_v_cache(expmc_matrix* m, int enable);
+int expmc_cuda_invalidate_v(expmc_matrix* m);
+int expmc_cuda_v_stagings(const expmc_matrix* m, uint64_t* count);
 /* vector_estimate (estimator.cpp:208-278), Theorem 2; values has n entries. */
 int expmc_cuda_vector_estimate(expmc_matrix* m, const double* v, uint64_t nv,
                                const expmc_path_params* p, double* values,

@@ -135,6 +135,39 @@ inline EntriesEstimate entries_estimate(const SplitMatrix& m, std::span<const do
     return out;
 }
 
+// Batched entry_estimate over several replicas of one matrix — the
+// reference's `workers` parallelism mapped to devices: `shards[k]` (one per
+// GPU, or several on one GPU) estimates the k-th contiguous block of rows,
+// all concurrently.  Bitwise identical to the single-replica call.
+inline EntriesEstimate entries_estimate(std::span<const SplitMatrix* const> shards,
+                                        std::span<const double> v,
+                                        std::span<const NodeId> rows, const PathParams& p) {
+    if (shards.empty()) throw std::invalid_argument("need at least one matrix handle");
+    const expmc_path_params c = p.c();
+    const std::size_t k = rows.empty() ? shards[0]->n() : rows.size();
+    std::vector<expmc_matrix*> hs;
+    for (const SplitMatrix* s : shards) hs.push_back(s ? s->handle() : nullptr);
+    EntriesEstimate out{std::vector<double>(k), std::vector<double>(k),
+                        std::vector<std::uint64_t>(k)};
+    check(expmc_cuda_entries_multi(hs.data(), (int)hs.size(), v.data(), v.size(),
+                                   rows.empty() ? nullptr : rows.data(), k, &c,
+                                   out.values.data(), out.std_errors.data(), out.jumps.data(),
+                                   &out.total_jumps));
+    return out;
+}
+
+// One replica per device 0..ndev-1 of the same symmetric CSR (the
+// `workers` -> GPUs mapping of entries_estimate above).
+inline std::vector<SplitMatrix> replicas(int ndev, std::size_t n,
+                                         std::span<const std::uint64_t> row_ptr,
+                                         std::span<const std::uint32_t> col,
+                                         std::span<const double> val,
+                                         std::span<const double> diag = {}) {
+    std::vector<SplitMatrix> r;
+    for (int d = 0; d < ndev; ++d) r.emplace_back(n, row_ptr, col, val, diag, d);
+    return r;
+}
+
 inline VectorEstimate vector_estimate(const SplitMatrix& m, std::span<const double> v,
                                       const PathParams& p, unsigned /*workers*/ = 1) {
     const expmc_path_params c = p.c();

@@ -54,6 +54,12 @@ SIGNATURES = [
      [vp, f64p, C.c_uint64, C.c_uint32, C.POINTER(PathParamsC), C.POINTER(EstimateC)]),
     ("expmc_cuda_entries", C.c_int,
      [vp, f64p, C.c_uint64, u32p, C.c_uint64, C.POINTER(PathParamsC), f64p, f64p, u64p, u64p]),
+    ("expmc_cuda_entries_multi", C.c_int,
+     [C.POINTER(vp), C.c_int, f64p, C.c_uint64, u32p, C.c_uint64, C.POINTER(PathParamsC), f64p,
+      f64p, u64p, u64p]),
+    ("expmc_cuda_set_v_cache", C.c_int, [vp, C.c_int]),
+    ("expmc_cuda_invalidate_v", C.c_int, [vp]),
+    ("expmc_cuda_v_stagings", C.c_int, [vp, u64p]),
     ("expmc_cuda_vector_estimate", C.c_int,
      [vp, f64p, C.c_uint64, C.POINTER(PathParamsC), f64p, f64p, u64p, f64p]),
     ("expmc_cuda_tc_estimate", C.c_int, [vp, C.POINTER(PathParamsC), C.POINTER(EstimateC)]),

@@ -13,6 +13,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -156,6 +158,18 @@ struct expmc_matrix {
     double d_lo = 0.0, d_hi = 0.0;  // range of d (K4 fixed-point scale), once
     bool d_range = false;
     DevBuf acc;
+    // One call at a time per handle: the scratch buffers, the packed v and
+    // the stream are per handle (the reference's SplitMatrix is shareable
+    // across threads; callers sharing a handle are serialised).
+    mutable std::mutex mu;
+    // Staged v (host entry calls): the packed RowRec.v / Edge.v / vdev hold
+    // the v of host pointer vkey_ptr (length vkey_n) when vstaged.  Reused
+    // without a copy only when the caller opted in (vcache, expmc_cuda_set_v_cache)
+    // and promises to call expmc_cuda_invalidate_v after changing v in place.
+    bool vcache = false, vstaged = false;
+    const double* vkey_ptr = nullptr;
+    uint64_t vkey_n = 0;
+    uint64_t v_stagings = 0;  // H2D + pack passes done (tests / measurement)
     // host copies kept for K5 norm bounds
     std::vector<double> h_rate, h_diag;
 
@@ -490,49 +504,27 @@ void run_entries_big(expmc_matrix* h, const uint32_t* rows_d, uint64_t nrows,
     void* scan_tmp = h->scan_tmp.get<unsigned char>(scan_bytes);
     launch_scan_u64(jc, off, nrows + 1, scan_tmp, scan_bytes, s);
     after_launch(2);
-    // fixed-point windows: |dev| <= F = 2 e^{β d_max} max|v|, so W F 2^s1 <
-    // 2^125 (signed) and W F^2 2^s2 < 2^126
-    unsigned long long* vmax_d = h->scal.get<unsigned long long>(4) + 3;
-    CK(cudaMemsetAsync(vmax_d, 0, 8, s));
-    launch_rec_v_absmax(h->m, vmax_d, s);
-    after_launch(1);
     uint64_t J = 0;
-    unsigned long long vbits = 0;
     CK(cudaMemcpyAsync(&J, off + nrows, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&vbits, vmax_d, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    double vmax;
-    std::memcpy(&vmax, &vbits, 8);
-    if (!h->d_range) {
-        std::vector<double> hd(h->m.n);
-        CK(cudaMemcpy(hd.data(), h->m.d, h->m.n * 8, cudaMemcpyDeviceToHost));
-        h->d_lo = *std::min_element(hd.begin(), hd.end());
-        h->d_hi = *std::max_element(hd.begin(), hd.end());
-        h->d_range = true;
-    }
-    const double lF = std::log2(vmax) + p->beta * h->d_hi / std::log(2.0) + 1.0;
-    // (the squares' window needs 2^(e2 - 64) to stay a normal double)
-    if (vmax > 0.0 && !(std::isfinite(lF) && lF < 480.0))
-        throw InvalidArg("samples >= 2^29 needs e^{beta max d} max|v| < 2^479");
-    const double lW = std::log2((double)W);
-    const int e1 = vmax > 0.0 ? std::min(1080, (int)std::floor(124.0 - lW - lF)) : 0;
-    const int e2 = vmax > 0.0 ? std::min(1080, (int)std::floor(125.0 - lW - 2.0 * lF)) : 0;
-    unsigned long long* acc1 = h->acc.get<unsigned long long>(4 * nrows);
-    unsigned long long* acc2 = acc1 + 2 * nrows;
-    CK(cudaMemsetAsync(acc1, 0, nrows * 32, s));
-    const uint64_t B = 1ull << 28;  // fixed (W >= 2^29), so repeated calls never regrow
+    // jumpers in batches of B; per batch, each jumper's dev and dev^2 go to
+    // records in q (= row) order and the deterministic run-sum passes add
+    // each row's run to s1 / s2 (batches in order: bitwise reproducible)
+    const uint64_t B = 1ull << 26;  // fixed, so repeated calls never regrow
     uint32_t* row_of = h->row_of.get<uint32_t>(B);
+    double* dev1 = h->acc.get<double>(2 * B);
+    double* dev2 = dev1 + B;
+    const size_t rs_bytes = run_sums_temp_bytes(B);
+    void* rs_tmp = h->sort_tmp.get<unsigned char>(rs_bytes);
     for (uint64_t q0 = 0; q0 < J; q0 += B) {
         const uint64_t q1 = std::min(J, q0 + B);
         launch_expand_rows(off, nrows, q0, q1, row_of, s);
-        launch_entry_big_walk(h->m, rows_d, rowc, Kr, row_of, off, fp, q0, q1,
-                              std::ldexp(1.0, e1 - 64), std::ldexp(1.0, e2 - 64), acc1, acc2,
-                              jr, s);
-        after_launch(2);
+        launch_entry_big_walk(h->m, rows_d, rowc, Kr, row_of, off, fp, q0, q1, dev1, dev2, jr,
+                              s);
+        run_sums_sorted(row_of, dev1, q1 - q0, rs_tmp, rs_bytes, s1, s);
+        run_sums_sorted(row_of, dev2, q1 - q0, rs_tmp, rs_bytes, s2, s);
+        after_launch(6);
     }
-    launch_entry_big_fold(nrows, acc1, acc2, std::ldexp(1.0, -e1), std::ldexp(1.0, -e2), s1, s2,
-                          s);
-    after_launch(1);
     launch_entry_big_finalize(nrows, W, Kr, s1, s2, jr, value, se, jumps, s);
     after_launch(1);
     CK(cudaGetLastError());
@@ -560,7 +552,14 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
     }
     // W >= 2^29 walkers per entry: the grouped large-W path (K3 packs walker
     // indices into 29 bits)
-    static const bool force_big = getenv("EXPMC_FORCE_BIG") != nullptr;  // experiments only
+#ifdef EXPMC_EXPERIMENTS
+    // experiment builds only (make variants): route W < 2^29 through the
+    // grouped path too — a different random-number contract, never in the
+    // shipped library
+    static const bool force_big = getenv("EXPMC_FORCE_BIG") != nullptr;
+#else
+    constexpr bool force_big = false;
+#endif
     const bool big = fast && (p->samples >= (1ull << 29) || force_big);
     if (nrows == 0) return;
     DeviceGuard g(h->device);
@@ -580,7 +579,13 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
     const auto t_host0 = std::chrono::steady_clock::now();
     mark(s);
     double* vd = h->vdev.get<double>(n);
-    CK(cudaMemcpyAsync(vd, v, n * 8, cudaMemcpyHostToDevice, s));
+    // staged-v reuse (opt-in): same host array, same length, nothing staged
+    // since — skip the H2D copy, the finiteness scan and the O(nnz) repack
+    const bool reuse = h->vcache && h->vstaged && v == h->vkey_ptr && nv == h->vkey_n;
+    if (!reuse) {
+        h->vstaged = false;
+        CK(cudaMemcpyAsync(vd, v, n * 8, cudaMemcpyHostToDevice, s));
+    }
     mark(s);
     if (fast) {
         // E2E path: device finiteness check, then the rows in pieces whose
@@ -591,10 +596,13 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
         unsigned int* flag = reinterpret_cast<unsigned int*>(sc);
         unsigned long long* jtot = sc + 1;
         CK(cudaMemsetAsync(sc, 0, 16, s));
-        launch_count_nonfinite(n, vd, flag, s);
-        launch_pack_v(n, vd, h->m.rec, s);
-        launch_pack_v_adj(h->m.nnz, h->m.neighbor, vd, h->m.adj, s);
-        after_launch(3);
+        if (!reuse) {
+            launch_count_nonfinite(n, vd, flag, s);
+            launch_pack_v(n, vd, h->m.rec, s);
+            launch_pack_v_adj(h->m.nnz, h->m.neighbor, vd, h->m.adj, s);
+            after_launch(3);
+            ++h->v_stagings;
+        }
         mark(s);
         if (nrows >= (1ull << 30)) throw InvalidArg("at most 2^30 rows per call");
         const uint32_t* rd;
@@ -620,6 +628,9 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
             CK(cudaStreamSynchronize(s));
             if ((unsigned int)res[0]) throw InvalidArg("non-finite entry in v");
             if (total_jumps) *total_jumps = res[1];
+            h->vstaged = true;
+            h->vkey_ptr = v;
+            h->vkey_n = nv;
             return;
         }
         static const int env_pieces = [] {
@@ -670,6 +681,9 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
         }
         if ((unsigned int)res[0]) throw InvalidArg("non-finite entry in v");
         if (total_jumps) *total_jumps = res[1];
+        h->vstaged = true;
+        h->vkey_ptr = v;
+        h->vkey_n = nv;
         return;
     }
     const uint32_t* rd;
@@ -1162,6 +1176,7 @@ int expmc_cuda_matrix_info(const expmc_matrix* h, uint64_t* n, uint64_t* nnz, do
                            uint64_t* dmax, int32_t* any_nonuniform, int32_t* device) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         if (n) *n = h->m.n;
         if (nnz) *nnz = h->m.nnz;
         if (dbar) *dbar = h->m.dbar;
@@ -1176,6 +1191,7 @@ int expmc_cuda_split_export(const expmc_matrix* h, double* diag, double* d, doub
                             double* cum, uint8_t* uniform_row) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         DeviceGuard g(h->device);
         const DevSplit& m = h->m;
         auto cp = [&](void* dst, const void* src, size_t bytes) {
@@ -1195,6 +1211,7 @@ int expmc_cuda_split_export(const expmc_matrix* h, double* diag, double* d, doub
 int expmc_cuda_alias_export(const expmc_matrix* h, uint32_t* thr, uint32_t* alias) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         DeviceGuard g(h->device);
         const DevSplit& m = h->m;
         if (!m.any_nonuniform) {  // uniform everywhere: identity tables
@@ -1215,6 +1232,7 @@ int expmc_cuda_alias_export(const expmc_matrix* h, uint32_t* thr, uint32_t* alia
 int expmc_cuda_records_export(const expmc_matrix* h, void* out) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         DeviceGuard g(h->device);
         if (h->m.n) CK(cudaMemcpy(out, h->m.rec, h->m.n * sizeof(RowRec), cudaMemcpyDeviceToHost));
     });
@@ -1224,6 +1242,7 @@ int expmc_cuda_entry_estimate(expmc_matrix* h, const double* v, uint64_t nv, uin
                               const expmc_path_params* p, expmc_estimate* out) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         validate_params(p);
         check_vector(h, v, nv);
         if (i >= h->m.n) throw InvalidArg("entry index out of range");
@@ -1242,6 +1261,7 @@ int expmc_cuda_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint
                        double* std_error, uint64_t* jumps, uint64_t* total_jumps) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         if (total_jumps) *total_jumps = 0;
         run_entries(h, v, nv, rows, nrows, p, value, std_error, jumps, total_jumps);
     });
@@ -1252,6 +1272,8 @@ int expmc_cuda_vector_estimate(expmc_matrix* h, const double* v, uint64_t nv,
                                double* std_error_global, uint64_t* total_jumps,
                                double* v_sum_out) {
     return guarded([&] {
+        std::unique_lock<std::mutex> lk;
+        if (h) lk = std::unique_lock<std::mutex>(h->mu);
         std::vector<double> cum;
         const double v_sum = vector_setup(h, v, nv, p, cum);
         double sum, sq;
@@ -1269,6 +1291,8 @@ int expmc_cuda_vector_estimate_rows(expmc_matrix* h, const double* v, uint64_t n
                                     uint64_t row_hi, double* values, double* sum,
                                     double* sum_sq, uint64_t* total_jumps) {
     return guarded([&] {
+        std::unique_lock<std::mutex> lk;
+        if (h) lk = std::unique_lock<std::mutex>(h->mu);
         std::vector<double> cum;
         const double v_sum = vector_setup(h, v, nv, p, cum);
         check_shard(h, p, row_lo, row_hi);
@@ -1282,6 +1306,7 @@ int expmc_cuda_tc_estimate_rows(expmc_matrix* h, const expmc_path_params* p, uin
                                 uint64_t* total_jumps) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         validate_params(p);
         if (h->m.n == 0) throw InvalidArg("empty matrix");  // estimator.cpp:283
         check_shard(h, p, row_lo, row_hi);
@@ -1293,6 +1318,7 @@ int expmc_cuda_tc_estimate_rows(expmc_matrix* h, const expmc_path_params* p, uin
 int expmc_cuda_tc_estimate(expmc_matrix* h, const expmc_path_params* p, expmc_estimate* out) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         validate_params(p);
         if (h->m.n == 0) throw InvalidArg("empty matrix");  // estimator.cpp:283
         double sum, sq;
@@ -1307,7 +1333,9 @@ int expmc_cuda_tc_estimate(expmc_matrix* h, const expmc_path_params* p, expmc_es
 int expmc_cuda_set_v_device(expmc_matrix* h, const double* v_dev, uint64_t nv, void* stream) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         if (nv != h->m.n) throw InvalidArg("vector length does not match matrix");
+        h->vstaged = false;  // the packed v now comes from device memory
         DeviceGuard g(h->device);
         cudaStream_t s = pick_stream(h, stream);
         unsigned int* flag = h->scal.get<unsigned int>(4);
@@ -1329,6 +1357,7 @@ int expmc_cuda_entries_device(expmc_matrix* h, const uint32_t* rows_dev, uint64_
                               double* std_error_dev, uint64_t* jumps_dev, void* stream) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         validate_params(p);
         if (p->rng != EXPMC_RNG_PHILOX)
             throw InvalidArg("entries_device supports the Philox walker only");
@@ -1348,9 +1377,92 @@ int expmc_cuda_entries_device(expmc_matrix* h, const uint32_t* rows_dev, uint64_
     });
 }
 
+int expmc_cuda_set_v_cache(expmc_matrix* h, int enable) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->vcache = enable != 0;
+        if (!h->vcache) h->vstaged = false;
+    });
+}
+
+int expmc_cuda_invalidate_v(expmc_matrix* h) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->vstaged = false;
+    });
+}
+
+int expmc_cuda_v_stagings(const expmc_matrix* h, uint64_t* count) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
+        if (count) *count = h->v_stagings;
+    });
+}
+
+int expmc_cuda_entries_multi(expmc_matrix* const* handles, int nh, const double* v, uint64_t nv,
+                             const uint32_t* rows, uint64_t nrows, const expmc_path_params* p,
+                             double* value, double* std_error, uint64_t* jumps,
+                             uint64_t* total_jumps) {
+    // Rows in nh contiguous, equal-count shards, shard k on
+    // handles[k] (one replica per GPU, or several handles on one GPU), each
+    // driven by its own host thread: the H2D of v, the walk and the D2H of
+    // the shard's slice straight into the caller's arrays run concurrently
+    // on all devices.  Keyed RNG + the fixed per-row reduction make the
+    // result bitwise identical to a single-handle call, for any nh.
+    return guarded([&] {
+        if (nh < 1 || !handles) throw InvalidArg("need at least one matrix handle");
+        for (int k = 0; k < nh; ++k) {
+            if (!handles[k]) throw InvalidArg("matrix handle is null");
+            if (handles[k]->m.n != handles[0]->m.n || handles[k]->m.nnz != handles[0]->m.nnz)
+                throw InvalidArg("shard handles hold different matrices");
+            for (int j = 0; j < k; ++j)
+                if (handles[j] == handles[k]) throw InvalidArg("shard handles must be distinct");
+        }
+        if (total_jumps) *total_jumps = 0;
+        const uint64_t n = handles[0]->m.n;
+        if (!rows && nrows != n) throw InvalidArg("rows == NULL requires nrows == n");
+        std::vector<uint32_t> iota;
+        const uint32_t* rr = rows;
+        if (!rows && nh > 1) {  // shards of the full vector need explicit rows
+            iota.resize(n);
+            for (uint64_t i = 0; i < n; ++i) iota[i] = (uint32_t)i;
+            rr = iota.data();
+        }
+        std::vector<int> rc(nh, EXPMC_OK);
+        std::vector<std::string> msg(nh);
+        std::vector<uint64_t> tj(nh, 0);
+        auto shard = [&](int k) {
+            const uint64_t lo = nrows * k / nh, hi = nrows * (k + 1) / nh;
+            rc[k] = guarded([&] {
+                std::lock_guard<std::mutex> lk(handles[k]->mu);
+                run_entries(handles[k], v, nv, rr ? rr + lo : nullptr, hi - lo, p, value + lo,
+                            std_error + lo, jumps + lo, &tj[k]);
+            });
+            if (rc[k] != EXPMC_OK) msg[k] = g_err;
+        };
+        std::vector<std::thread> pool;
+        for (int k = 1; k < nh; ++k) pool.emplace_back(shard, k);
+        shard(0);
+        for (auto& t : pool) t.join();
+        for (int k = 0; k < nh; ++k)
+            if (rc[k] != EXPMC_OK) {
+                g_err = msg[k];
+                if (rc[k] == EXPMC_INVALID_ARGUMENT) throw InvalidArg(msg[k]);
+                if (rc[k] == EXPMC_CUDA_ERROR) throw CudaErr(msg[k]);
+                throw std::runtime_error(msg[k]);
+            }
+        if (total_jumps)
+            for (uint64_t t : tj) *total_jumps += t;
+    });
+}
+
 int expmc_cuda_last_k4_stats(const expmc_matrix* h, uint64_t* jumpers, int* fixed_point) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         if (jumpers) *jumpers = h->last_jumpers;
         if (fixed_point) *fixed_point = h->last_fixed;
     });
@@ -1377,6 +1489,7 @@ int expmc_cuda_start_counts(expmc_matrix* h, const double* v, uint64_t nv, uint6
                             uint64_t seed, uint64_t* counts) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         if (!counts) throw InvalidArg("counts is null");
         DeviceGuard g(h->device);
         cudaStream_t s = h->stream;
@@ -1421,6 +1534,7 @@ int expmc_cuda_gather_ceiling_device(expmc_matrix* h, const uint32_t* rows_dev, 
                                      void* stream) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         DeviceGuard g(h->device);
         unsigned long long* sink = h->scal.get<unsigned long long>(4);
         launch_gather_ceiling(h->m, rows_dev, nrows, chains_per_row, chain_len, 0x2545F491u,
@@ -1433,6 +1547,7 @@ int expmc_cuda_expmv(expmc_matrix* h, const double* v, uint64_t nv, double t, do
                      double* out) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         check_vector(h, v, nv);
         if (!std::isfinite(t)) throw InvalidArg("t must be finite");
         if (!(tol > 0.0)) throw InvalidArg("tol must be positive");
@@ -1453,6 +1568,7 @@ int expmc_cuda_lambda_max(expmc_matrix* h, uint64_t power_iters, double* lambda_
     // shifted by its Gershgorin lower bound), on the device.
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         const uint64_t n = h->m.n;
         *lambda_max = 0.0;
         if (rel_change) *rel_change = 0.0;
@@ -1506,6 +1622,7 @@ int expmc_cuda_splitting_product(expmc_matrix* h, const double* v, uint64_t nv,
                                  const expmc_path_params* p, double tol, double* out) {
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
         validate_params(p);
         check_vector(h, v, nv);
         if (!(tol > 0.0)) throw InvalidArg("tol must be positive");

@@ -143,13 +143,8 @@ void launch_entry_big_rows(const DevSplit& m, const uint32_t* rows, uint64_t nro
                            double* s1, double* s2, unsigned long long* jumps, cudaStream_t s);
 void launch_entry_big_walk(const DevSplit& m, const uint32_t* rows, const double2* rowc,
                            const double* Kr, const uint32_t* row_of, const uint64_t* off,
-                           const FastParams& p, uint64_t q0, uint64_t q1, double sc1_hi,
-                           double sc2_hi, unsigned long long* acc1, unsigned long long* acc2,
-                           unsigned long long* jumps, cudaStream_t s);
-void launch_entry_big_fold(uint64_t nrows, const unsigned long long* acc1,
-                           const unsigned long long* acc2, double inv1, double inv2, double* s1,
-                           double* s2, cudaStream_t s);
-void launch_rec_v_absmax(const DevSplit& m, unsigned long long* out, cudaStream_t s);
+                           const FastParams& p, uint64_t q0, uint64_t q1, double* dev1,
+                           double* dev2, unsigned long long* jumps, cudaStream_t s);
 void launch_entry_big_finalize(uint64_t nrows, uint64_t W, const double* Kr, const double* s1,
                                const double* s2, const unsigned long long* jumps, double* value,
                                double* se, uint64_t* out_jumps, cudaStream_t s);

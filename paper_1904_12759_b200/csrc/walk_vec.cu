@@ -457,20 +457,21 @@ __global__ void entry_big_rows_kernel(const uint32_t* __restrict__ rows, uint64_
     }
 }
 
-// Jumper walks of the large-W entry path.  Each lane keeps exact 128-bit
-// fixed-point sums of dev = f - K_r and dev^2 for the row its jumpers come
-// from (static grid-stride assignment: a lane's consecutive jumpers share a
-// row unless the stride crosses a row boundary) and flushes them with
-// integer atomics when the row changes: exact and order-independent, so
-// deterministic whatever the scheduling.
+// Jumper walks of the large-W entry path.  Jumper q of the batch [q0, q1)
+// writes its deviation dev = f - K_r and dev^2 to records q - q0; the
+// records are in row order (q numbers a row's jumpers consecutively), and
+// the host sums them per row with the deterministic run-sum passes
+// (scatter_sort.cu run_sums_sorted: fixed 32-record pieces, pieces in
+// order, batches in order) — no fixed-point window, so rows of any scale
+// keep full fp64 resolution whatever the largest e^{beta d} of the matrix.
+// Jump counts: exact integer atomics.
 __global__ void __launch_bounds__(128)
 entry_big_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj,
                       const uint32_t* __restrict__ thr, const uint32_t* __restrict__ alias,
                       const uint32_t* __restrict__ rows, const double2* __restrict__ rowc,
                       const double* __restrict__ Kr, const uint32_t* __restrict__ row_of,
                       const uint64_t* __restrict__ off, FastParams p, uint64_t q0, uint64_t q1,
-                      double sc1_hi, double sc2_hi, unsigned long long* __restrict__ acc1,
-                      unsigned long long* __restrict__ acc2,
+                      double* __restrict__ dev1, double* __restrict__ dev2,
                       unsigned long long* __restrict__ jumps) {
     const uint64_t stride = blockDim.x;  // block-owned ranges, as vec_walk_kernel
     const uint64_t qb0 = q0 + blockIdx.x * (uint64_t)blockDim.x * kPer;
@@ -481,22 +482,15 @@ entry_big_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ a
     uint32_t r = 0, i = 0, off_c = 0, degf = 0, step = 0, jc = 0, klo = 0, tagv = 0;
     float ir = 0.f;
     double dcur = 0.0, vcur = 0.0, t = 0.0, S = 0.0, g = 0.0, corr0 = 0.0, K = 0.0;
-    uint32_t ar = 0xffffffffu;  // row of the lane's open sums
-    U128 a1{0, 0}, a2{0, 0};
+    uint32_t ar = 0xffffffffu;  // row of the lane's open jump count
     unsigned long long aj = 0;
     while (true) {
         if (!active) {
             if (q >= q1) break;
             r = __ldg(row_of + (q - q0));
             if (r != ar) {
-                if (ar != 0xffffffffu) {
-                    flush128(acc1, ar, a1);
-                    flush128(acc2, ar, a2);
-                    if (aj) atomicAdd(jumps + ar, aj);
-                }
+                if (ar != 0xffffffffu && aj) atomicAdd(jumps + ar, aj);
                 ar = r;
-                a1 = U128{0, 0};
-                a2 = U128{0, 0};
                 aj = 0;
             }
             i = __ldg(rows + r);
@@ -532,8 +526,8 @@ entry_big_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ a
             const double Sx = p.strang ? __dsub_rn(S, __dmul_rn(0.5, dcur)) : S;
             const double f = __dmul_rn(exp(__dmul_rn(p.dt, __dsub_rn(Sx, corr0))), vcur);
             const double dv = __dsub_rn(f, K);
-            add128(a1, to_fixed(dv, sc1_hi));
-            add128(a2, to_fixed(__dmul_rn(dv, dv), sc2_hi));
+            dev1[q - q0] = dv;
+            dev2[q - q0] = __dmul_rn(dv, dv);
             aj += jc;
             active = false;
             q += stride;
@@ -548,44 +542,7 @@ entry_big_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ a
             ++step;
         }
     }
-    if (ar != 0xffffffffu) {
-        flush128(acc1, ar, a1);
-        flush128(acc2, ar, a2);
-        if (aj) atomicAdd(jumps + ar, aj);
-    }
-}
-
-// s1 += (signed 128-bit acc1) 2^-s1, s2 += acc2 2^-s2 (one rounding each)
-__global__ void entry_big_fold_kernel(uint64_t nrows, const unsigned long long* __restrict__ acc1,
-                                      const unsigned long long* __restrict__ acc2,
-                                      double inv1, double inv2, double* __restrict__ s1,
-                                      double* __restrict__ s2) {
-    const uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (r >= nrows) return;
-    unsigned long long lo = acc1[2 * r], hi = acc1[2 * r + 1];
-    const bool neg = (long long)hi < 0;
-    if (neg) {
-        lo = ~lo + 1ull;
-        hi = ~hi + (lo == 0ull ? 1ull : 0ull);
-    }
-    double x = __fma_rn(__ull2double_rn(hi), 0x1.0p64, __ull2double_rn(lo));
-    x = __dmul_rn(neg ? -x : x, inv1);
-    s1[r] = __dadd_rn(s1[r], x);
-    const double y = __fma_rn(__ull2double_rn(acc2[2 * r + 1]), 0x1.0p64,
-                              __ull2double_rn(acc2[2 * r]));
-    s2[r] = __dadd_rn(s2[r], __dmul_rn(y, inv2));
-}
-
-// max |v| over the packed row records (bit patterns of non-negative doubles
-// order like unsigned integers)
-__global__ void rec_v_absmax_kernel(const RowRec* __restrict__ rec, uint64_t n,
-                                    unsigned long long* __restrict__ out) {
-    unsigned long long m = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        m = max(m, (unsigned long long)__double_as_longlong(fabs(rec[i].v)));
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+    if (ar != 0xffffffffu && aj) atomicAdd(jumps + ar, aj);
 }
 
 // value = K + Σdev / W, SE from the one-pass variance of the deviations
@@ -698,25 +655,13 @@ void launch_entry_big_rows(const DevSplit& m, const uint32_t* rows, uint64_t nro
 
 void launch_entry_big_walk(const DevSplit& m, const uint32_t* rows, const double2* rowc,
                            const double* Kr, const uint32_t* row_of, const uint64_t* off,
-                           const FastParams& p, uint64_t q0, uint64_t q1, double sc1_hi,
-                           double sc2_hi, unsigned long long* acc1, unsigned long long* acc2,
-                           unsigned long long* jumps, cudaStream_t s) {
+                           const FastParams& p, uint64_t q0, uint64_t q1, double* dev1,
+                           double* dev2, unsigned long long* jumps, cudaStream_t s) {
     entry_big_walk_kernel<<<vec_walk_blocks(q1 - q0), 128, 0, s>>>(m.rec, m.adj, m.alias_thr,
                                                           m.alias_idx, rows, rowc, Kr, row_of,
-                                                          off, p, q0, q1, sc1_hi, sc2_hi, acc1,
-                                                          acc2, jumps);
+                                                          off, p, q0, q1, dev1, dev2, jumps);
 }
 
-void launch_entry_big_fold(uint64_t nrows, const unsigned long long* acc1,
-                           const unsigned long long* acc2, double inv1, double inv2, double* s1,
-                           double* s2, cudaStream_t s) {
-    entry_big_fold_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(nrows, acc1, acc2,
-                                                                          inv1, inv2, s1, s2);
-}
-
-void launch_rec_v_absmax(const DevSplit& m, unsigned long long* out, cudaStream_t s) {
-    rec_v_absmax_kernel<<<148 * 4, 256, 0, s>>>(m.rec, m.n, out);
-}
 
 void launch_entry_big_finalize(uint64_t nrows, uint64_t W, const double* Kr, const double* s1,
                                const double* s2, const unsigned long long* jumps, double* value,

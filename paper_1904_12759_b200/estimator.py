@@ -282,6 +282,54 @@ def entries_estimate(m: SplitMatrix, v, rows, p: PathParams, out=None) -> Entrie
     return EntriesEstimate(rows_arr, val, se, jm, p.samples, tot.value)
 
 
+def entries_estimate_multi(ms, v, rows, p: PathParams, out=None) -> EntriesEstimate:
+    """Batched entry_estimate over several replicas (one per GPU, or several
+    on one GPU): rows in len(ms) contiguous equal shards, all run
+    concurrently (C ABI expmc_cuda_entries_multi).  Bitwise identical to
+    :func:`entries_estimate` on one replica."""
+    ms = list(ms)
+    if not ms:
+        raise ValueError("need at least one matrix")
+    v = _f64(v)
+    pc = p._c()
+    n = ms[0].n
+    if rows is None:
+        nrows, rp, rows_arr = n, None, None
+    else:
+        rows_arr = np.asarray(rows)
+        if rows_arr.size and (rows_arr.min() < 0 or rows_arr.max() >= 2**32):
+            raise ValueError("entry index out of range")
+        rows_arr = np.ascontiguousarray(rows_arr, dtype=np.uint32)
+        nrows, rp = len(rows_arr), rows_arr.ctypes.data_as(u32p)
+    if out is None:
+        val, se, jm = np.zeros(nrows), np.zeros(nrows), np.zeros(nrows, np.uint64)
+    else:
+        val, se, jm = out
+    hs = (C.c_void_p * len(ms))(*[m.handle for m in ms])
+    tot = C.c_uint64()
+    check(lib().expmc_cuda_entries_multi(hs, len(ms), v.ctypes.data_as(f64p), len(v), rp, nrows,
+                                         C.byref(pc), val.ctypes.data_as(f64p),
+                                         se.ctypes.data_as(f64p), jm.ctypes.data_as(u64p),
+                                         C.byref(tot)))
+    return EntriesEstimate(rows_arr, val, se, jm, p.samples, tot.value)
+
+
+def set_v_cache(m: SplitMatrix, enable: bool = True) -> None:
+    """Reuse the staged v across host entry calls with the same array (call
+    :func:`invalidate_v` after changing it in place)."""
+    check(lib().expmc_cuda_set_v_cache(m.handle, 1 if enable else 0))
+
+
+def invalidate_v(m: SplitMatrix) -> None:
+    check(lib().expmc_cuda_invalidate_v(m.handle))
+
+
+def v_stagings(m: SplitMatrix) -> int:
+    c = C.c_uint64()
+    check(lib().expmc_cuda_v_stagings(m.handle, C.byref(c)))
+    return int(c.value)
+
+
 def vector_estimate(m: SplitMatrix, v, p: PathParams, workers: int = 1) -> VectorEstimate:
     """estimator.cpp:208-278 — Theorem 2 full-vector estimator (v >= 0)."""
     v = _f64(v)

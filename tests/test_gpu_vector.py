@@ -334,6 +334,51 @@ def test_entries_beyond_2_29_walkers(pb, splitting):
     assert e.std_error == pytest.approx(big.std_errors[3], rel=1e-9)
 
 
+def test_entries_beyond_2_29_walkers_hub_and_leaf_rows(pb):
+    """Regression (round-1 advisor finding): the W >= 2^29 path once summed
+    in a 128-bit fixed-point window sized from e^{beta d_max} max|v| of the
+    whole matrix; with a hub at e^{beta d} ~ 1e139 every O(1) deviation of an
+    ordinary row truncated to 0 (value = K, SE = 0).  Now each row's
+    deviations are summed in fp64 by the deterministic run-sum passes.
+    Ordinary rows of a small component next to a 2000-leaf star hub: W = 2^29
+    against K3 at W = 2^25 and against the splitting product."""
+    D = 2000
+    n = D + 1 + 5
+    rows_, cols_, w_ = [], [], []
+    for k in range(1, D + 1):  # star: hub 0, leaves 1..D
+        rows_ += [0, k]
+        cols_ += [k, 0]
+        w_ += [1.0, 1.0]
+    path = list(range(D + 1, n))  # a separate 5-node weighted path
+    for a, b, w in zip(path[:-1], path[1:], [1.0, 0.5, 2.0, 1.5]):
+        rows_ += [a, b]
+        cols_ += [b, a]
+        w_ += [w, w]
+    order = np.lexsort((np.array(cols_), np.array(rows_)))
+    r_, c_, ww = np.array(rows_)[order], np.array(cols_)[order], np.array(w_)[order]
+    rp = np.zeros(n + 1, np.uint64)
+    np.add.at(rp, r_ + 1, 1)
+    rp = np.cumsum(rp).astype(np.uint64)
+    csr = pb.Csr(n, rp, c_.astype(np.uint32), ww, np.zeros(n))
+    m = pb.split(csr)
+    v = np.ones(n)
+    v[path] = [0.3, -1.0, 0.8, 0.5, -0.2]
+    beta = 0.16  # hub: e^{beta d} = e^{320}
+    rows = np.array(path, np.uint32)
+    big = pb.entries_estimate(m, v, rows, pb.PathParams(beta, 32, 1 << 29, pb.Splitting.Strang, 7))
+    Ws = 1 << 25
+    small = pb.entries_estimate(m, v, rows, pb.PathParams(beta, 32, Ws, pb.Splitting.Strang, 8))
+    x = pb.splitting_product(m, v, pb.PathParams(beta, 32, 10, pb.Splitting.Strang))[path]
+    assert np.all(big.std_errors > 0), big.std_errors
+    z = (big.values - small.values) / np.sqrt(big.std_errors ** 2 + small.std_errors ** 2)
+    assert np.all(np.abs(z) < 5), z
+    assert np.all(np.abs((big.values - x) / big.std_errors) < 5)
+    # the hub row itself: every walker leaves at once (K = 0), huge values
+    hub = pb.entries_estimate(m, v, np.array([0], np.uint32),
+                              pb.PathParams(beta, 32, 1 << 29, pb.Splitting.Strang, 7))
+    assert np.isfinite(hub.values[0]) and hub.std_errors[0] > 0
+
+
 @pytest.mark.parametrize("M", [1, 2, 3, 33, 1000])
 def test_small_sample_counts(pb, ref, M):
     """Tiny M (down to one walker): the start tree, the never-jumper split
