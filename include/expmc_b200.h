@@ -142,6 +142,12 @@ int expmc_cuda_entries_multi(expmc_matrix* const* handles, int nh, const double*
 int expmc_cuda_set_v_cache(expmc_matrix* m, int enable);
 int expmc_cuda_invalidate_v(expmc_matrix* m);
 int expmc_cuda_v_stagings(const expmc_matrix* m, uint64_t* count);
+/* Test hook: `count` Exp(1) draws of the walkers' transform (neg_ln_u over
+ * Philox words), histogram in nbins bins of bin_width (last bin = the rest)
+ * and moments {sum E, sum E^2}; the law check of sampler.cpp:10-16's
+ * exp_time (tests/test_gpu_rng_law.py). */
+int expmc_cuda_exp_law(int device, uint64_t count, uint64_t seed, double bin_width,
+                       uint32_t nbins, uint64_t* hist, double* moments);
 /* vector_estimate (estimator.cpp:208-278), Theorem 2; values has n entries. */
 int expmc_cuda_vector_estimate(expmc_matrix* m, const double* v, uint64_t nv,
                                const expmc_path_params* p, double* values,

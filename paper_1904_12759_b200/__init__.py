@@ -9,7 +9,7 @@ from ._lib import ExpmcError, lib
 from .estimator import (EntriesEstimate, binomial_samples, last_jumpers, last_k4_stats, start_counts, tc_estimate_rows,
                         vector_estimate_rows, finalize, Estimate, PathParams, Rng, SplitMatrix, Splitting,
                         VectorEstimate, entries_device, entries_estimate, entries_estimate_multi, entry_estimate,
-                        invalidate_v, set_v_cache, v_stagings,
+                        invalidate_v, set_v_cache, v_stagings, exp_law,
                         entry_slots, expmv, from_entries, from_matrix_market, gather_ceiling_device, launch_count, set_v_device,
                         split, splitting_product, tc_estimate, vector_estimate)
 from .inputs import (Csr, MmEntries, build_config, csr_from_dense, gen_ba, gen_fd, gen_row_sample,
@@ -21,7 +21,7 @@ __all__ = [
     "ExpmcError", "lib", "binomial_samples", "last_jumpers", "last_k4_stats", "start_counts", "tc_estimate_rows",
     "vector_estimate_rows", "finalize", "EntriesEstimate", "Estimate", "PathParams", "Rng", "SplitMatrix",
     "Splitting", "VectorEstimate", "entries_device", "entries_estimate", "entries_estimate_multi",
-    "entry_estimate", "invalidate_v", "set_v_cache", "v_stagings",
+    "entry_estimate", "invalidate_v", "set_v_cache", "v_stagings", "exp_law",
     "entry_slots", "expmv", "gather_ceiling_device", "launch_count", "set_v_device", "split",
     "splitting_product", "tc_estimate", "vector_estimate", "Csr", "build_config",
     "csr_from_dense", "gen_ba", "gen_fd", "gen_row_sample", "gen_vector", "gen_ws", "n_rule",

@@ -57,6 +57,8 @@ SIGNATURES = [
     ("expmc_cuda_entries_multi", C.c_int,
      [C.POINTER(vp), C.c_int, f64p, C.c_uint64, u32p, C.c_uint64, C.POINTER(PathParamsC), f64p,
       f64p, u64p, u64p]),
+    ("expmc_cuda_exp_law", C.c_int,
+     [C.c_int, C.c_uint64, C.c_uint64, C.c_double, C.c_uint32, u64p, f64p]),
     ("expmc_cuda_set_v_cache", C.c_int, [vp, C.c_int]),
     ("expmc_cuda_invalidate_v", C.c_int, [vp]),
     ("expmc_cuda_v_stagings", C.c_int, [vp, u64p]),

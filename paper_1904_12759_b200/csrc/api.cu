@@ -544,11 +544,34 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
         check_vector(h, v, nv);
     }
     const uint64_t n = h->m.n;
+    bool bad_row = false;
     if (rows) {
         for (uint64_t r = 0; r < nrows; ++r)
-            if (rows[r] >= n) throw InvalidArg("entry index out of range");
+            if (rows[r] >= n) {
+                bad_row = true;
+                break;
+            }
     } else if (nrows != n) {
         throw InvalidArg("rows == NULL requires nrows == n");
+    }
+    if (bad_row) {
+        // the reference checks v before the index (estimator.cpp:172-173):
+        // a non-finite v wins, found by the device scan the Philox path uses
+        if (fast && n) {
+            DeviceGuard g(h->device);
+            double* vd = h->vdev.get<double>(n);
+            unsigned int* flag = h->scal.get<unsigned int>(4);
+            h->vstaged = false;
+            CK(cudaMemcpyAsync(vd, v, n * 8, cudaMemcpyHostToDevice, h->stream));
+            CK(cudaMemsetAsync(flag, 0, 4, h->stream));
+            launch_count_nonfinite(n, vd, flag, h->stream);
+            after_launch(1);
+            unsigned int bad = 0;
+            CK(cudaMemcpyAsync(&bad, flag, 4, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            if (bad) throw InvalidArg("non-finite entry in v");
+        }
+        throw InvalidArg("entry index out of range");
     }
     // W >= 2^29 walkers per entry: the grouped large-W path (K3 packs walker
     // indices into 29 bits)
@@ -1243,9 +1266,9 @@ int expmc_cuda_entry_estimate(expmc_matrix* h, const double* v, uint64_t nv, uin
     return guarded([&] {
         if (!h) throw InvalidArg("matrix handle is null");
         std::lock_guard<std::mutex> lk(h->mu);
-        validate_params(p);
-        check_vector(h, v, nv);
-        if (i >= h->m.n) throw InvalidArg("entry index out of range");
+        // run_entries applies the reference's checks in its order
+        // (estimator.cpp:171-173); the Philox path scans v for finiteness on
+        // the device when it stages v, not with an O(n) host loop per call
         double val, se;
         uint64_t j;
         run_entries(h, v, nv, &i, 1, p, &val, &se, &j);
@@ -1382,7 +1405,7 @@ int expmc_cuda_set_v_cache(expmc_matrix* h, int enable) {
         if (!h) throw InvalidArg("matrix handle is null");
         std::lock_guard<std::mutex> lk(h->mu);
         h->vcache = enable != 0;
-        if (!h->vcache) h->vstaged = false;
+        h->vstaged = false;  // the first call after (re-)enabling stages v
     });
 }
 
@@ -1456,6 +1479,27 @@ int expmc_cuda_entries_multi(expmc_matrix* const* handles, int nh, const double*
             }
         if (total_jumps)
             for (uint64_t t : tj) *total_jumps += t;
+    });
+}
+
+int expmc_cuda_exp_law(int device, uint64_t count, uint64_t seed, double bin_width,
+                       uint32_t nbins, uint64_t* hist, double* moments) {
+    return guarded([&] {
+        if (count % 4 || nbins < 2 || nbins > 8192 || !(bin_width > 0.0) || !hist || !moments)
+            throw InvalidArg("exp_law: needs count % 4 == 0, 2 <= nbins <= 8192, width > 0");
+        DeviceGuard g(device);
+        unsigned long long* d = nullptr;
+        CK(cudaMalloc(&d, (nbins + 2) * sizeof(unsigned long long)));
+        CK(cudaMemset(d, 0, (nbins + 2) * sizeof(unsigned long long)));
+        launch_exp_law(count, seed, bin_width, nbins, d, d + nbins, nullptr);
+        after_launch(1);
+        std::vector<unsigned long long> hv(nbins + 2);
+        const cudaError_t e = cudaMemcpy(hv.data(), d, hv.size() * 8, cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        CK(e);
+        for (uint32_t b = 0; b < nbins; ++b) hist[b] = hv[b];
+        moments[0] = std::ldexp((double)hv[nbins], -30);
+        moments[1] = std::ldexp((double)hv[nbins + 1], -30);
     });
 }
 

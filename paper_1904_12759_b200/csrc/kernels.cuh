@@ -111,6 +111,8 @@ size_t entry_fast_scratch_bytes(uint64_t nrows, uint64_t W);
 int launch_entry_fast(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
                       const FastParams& p, double* value, double* se, uint64_t* jumps,
                       void* scratch, cudaStream_t s);
+void launch_exp_law(uint64_t count, uint64_t seed, double width, uint32_t nbins,
+                    unsigned long long* hist, unsigned long long* mom, cudaStream_t s);
 void launch_gather_ceiling(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
                            uint32_t chains_per_row, uint32_t chain_len, uint32_t salt,
                            unsigned long long* sink, cudaStream_t s);

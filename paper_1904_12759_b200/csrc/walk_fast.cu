@@ -43,7 +43,47 @@ gather_ceiling_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ a
     if (acc == 0x7fffffffffffffffull) *sink = acc;  // keep the loads live
 }
 
+// Law check of the walkers' Exp(1) transform (test hook): 4 count Philox
+// words (counters (k, 0, 0, 'LAWS')) through neg_ln_u, histogrammed in bins
+// of `width` (the last bin collects the rest) with the raw sum and sum of
+// squares (integer atomics: exact, order-independent).
+__global__ void exp_law_kernel(uint64_t blocks, PhiloxKeys K, double width, uint32_t nbins,
+                               unsigned long long* __restrict__ hist,
+                               unsigned long long* __restrict__ mom) {
+    extern __shared__ unsigned int sh[];  // per-block histogram (u32: < 2^32 per block)
+    for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) sh[b] = 0u;
+    __syncthreads();
+    unsigned long long s1 = 0, s2 = 0;  // sums of E and E^2 in 2^-30 units
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < blocks;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const U4 w = philox4x32_10(U4{(uint32_t)k, (uint32_t)(k >> 32), 0u, 0x4c415753u}, K);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float E = neg_ln_u(ws[q]);
+            uint32_t b = (uint32_t)((double)E / width);
+            b = b < nbins - 1 ? b : nbins - 1;
+            atomicAdd(sh + b, 1u);
+            s1 += (unsigned long long)((double)E * 1073741824.0);
+            s2 += (unsigned long long)((double)E * (double)E * 1073741824.0);
+        }
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x)
+        if (sh[b]) atomicAdd(hist + b, (unsigned long long)sh[b]);
+    atomicAdd(mom, s1);
+    atomicAdd(mom + 1, s2);
+}
+
 }  // namespace
+
+void launch_exp_law(uint64_t count, uint64_t seed, double width, uint32_t nbins,
+                    unsigned long long* hist, unsigned long long* mom, cudaStream_t s) {
+    const uint64_t blocks = count / 4;
+    const PhiloxKeys K = philox_keys((uint32_t)seed, (uint32_t)(seed >> 32));
+    exp_law_kernel<<<148 * 8, 256, nbins * sizeof(unsigned int), s>>>(blocks, K, width, nbins,
+                                                                    hist, mom);
+}
 
 void launch_gather_ceiling(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
                            uint32_t chains_per_row, uint32_t chain_len, uint32_t salt,

@@ -424,6 +424,17 @@ def gather_ceiling_device(m: SplitMatrix, rows_ptr: int, nrows: int, chains_per_
                                                  stream or None))
 
 
+def exp_law(count: int, seed: int = 0, bin_width: float = 0.05, nbins: int = 512, device=0):
+    """Test hook: histogram + moments of `count` draws of the walkers' Exp(1)
+    transform (neg_ln_u over Philox words)."""
+    hist = np.zeros(int(nbins), np.uint64)
+    mom = np.zeros(2)
+    check(lib().expmc_cuda_exp_law(int(device), int(count), int(seed), float(bin_width),
+                                   int(nbins), hist.ctypes.data_as(u64p),
+                                   mom.ctypes.data_as(f64p)))
+    return hist, mom
+
+
 def last_k4_stats(m: SplitMatrix):
     """(jumpers, fixed_point) of the last vector / tc call on m: walks K4
     actually ran, and whether vector_estimate's per-end sums used the exact
