@@ -28,7 +28,16 @@ using namespace expmc_b200;
 
 namespace {
 
-thread_local std::string g_err;
+// Last error message of this thread.  A trivially destructible buffer, not
+// a std::string: a handle destroyed during static destruction (a cache of
+// device copies in a caller's static map) may report an error after the
+// thread's thread_local destructors have run.
+struct ErrSlot {
+    char s[2048];
+};
+thread_local ErrSlot g_err_slot;
+void set_err(const char* m) { std::snprintf(g_err_slot.s, sizeof g_err_slot.s, "%s", m); }
+void set_err(const std::string& m) { set_err(m.c_str()); }
 std::atomic<uint64_t> g_launches{0};
 
 struct InvalidArg : std::invalid_argument {
@@ -56,16 +65,16 @@ int guarded(F&& f) {
         f();
         return EXPMC_OK;
     } catch (const CudaErr& e) {
-        g_err = e.what();
+        set_err(e.what());
         return EXPMC_CUDA_ERROR;
     } catch (const std::invalid_argument& e) {
-        g_err = e.what();
+        set_err(e.what());
         return EXPMC_INVALID_ARGUMENT;
     } catch (const std::exception& e) {
-        g_err = e.what();
+        set_err(e.what());
         return EXPMC_RUNTIME_ERROR;
     } catch (...) {
-        g_err = "unknown error";
+        set_err("unknown error");
         return EXPMC_RUNTIME_ERROR;
     }
 }
@@ -1064,7 +1073,7 @@ void check_shard(const expmc_matrix* h, const expmc_path_params* p, uint64_t lo,
 
 extern "C" {
 
-const char* expmc_cuda_last_error(void) { return g_err.c_str(); }
+const char* expmc_cuda_last_error(void) { return g_err_slot.s; }
 int expmc_cuda_abi_version(void) { return 1; }
 uint64_t expmc_cuda_launch_count(void) { return g_launches.load(); }
 uint32_t expmc_cuda_entry_slots(uint64_t walkers) {
@@ -1464,7 +1473,7 @@ int expmc_cuda_entries_multi(expmc_matrix* const* handles, int nh, const double*
                 run_entries(handles[k], v, nv, rr ? rr + lo : nullptr, hi - lo, p, value + lo,
                             std_error + lo, jumps + lo, &tj[k]);
             });
-            if (rc[k] != EXPMC_OK) msg[k] = g_err;
+            if (rc[k] != EXPMC_OK) msg[k] = g_err_slot.s;
         };
         std::vector<std::thread> pool;
         for (int k = 1; k < nh; ++k) pool.emplace_back(shard, k);
@@ -1472,7 +1481,7 @@ int expmc_cuda_entries_multi(expmc_matrix* const* handles, int nh, const double*
         for (auto& t : pool) t.join();
         for (int k = 0; k < nh; ++k)
             if (rc[k] != EXPMC_OK) {
-                g_err = msg[k];
+                set_err(msg[k]);
                 if (rc[k] == EXPMC_INVALID_ARGUMENT) throw InvalidArg(msg[k]);
                 if (rc[k] == EXPMC_CUDA_ERROR) throw CudaErr(msg[k]);
                 throw std::runtime_error(msg[k]);

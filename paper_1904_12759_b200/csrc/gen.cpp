@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -20,10 +21,14 @@
 #include "host_io.h"
 
 namespace expmc_b200 {
-std::string& host_error() {
-    thread_local std::string msg;
-    return msg;
-}
+namespace {
+struct HostErr {
+    char s[2048];
+};
+thread_local HostErr g_host_err;
+}  // namespace
+void set_host_error(const char* m) { std::snprintf(g_host_err.s, sizeof g_host_err.s, "%s", m); }
+const char* host_error_str() { return g_host_err.s; }
 }  // namespace expmc_b200
 
 namespace {
@@ -88,7 +93,7 @@ expmc_csr* csr_from_edges(uint64_t n, const std::vector<uint32_t>& ea,
 
 extern "C" {
 
-const char* expmc_gen_last_error(void) { return expmc_b200::host_error().c_str(); }
+const char* expmc_gen_last_error(void) { return expmc_b200::host_error_str(); }
 
 int expmc_gen_fd(int dim, uint64_t side, double s, expmc_csr** out) {
     return guarded([&] {

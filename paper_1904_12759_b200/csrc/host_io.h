@@ -35,8 +35,11 @@ struct expmc_mm {
 
 namespace expmc_b200 {
 
-// Message slot behind expmc_gen_last_error() (thread-local).
-std::string& host_error();
+// Message slot behind expmc_gen_last_error() (thread-local, trivially
+// destructible so that late errors during exit cannot touch a destroyed
+// string).
+void set_host_error(const char* m);
+const char* host_error_str();
 
 template <class F>
 int host_guarded(F&& f) {
@@ -44,13 +47,13 @@ int host_guarded(F&& f) {
         f();
         return EXPMC_OK;
     } catch (const std::invalid_argument& e) {
-        host_error() = e.what();
+        set_host_error(e.what());
         return EXPMC_INVALID_ARGUMENT;
     } catch (const std::exception& e) {
-        host_error() = e.what();
+        set_host_error(e.what());
         return EXPMC_RUNTIME_ERROR;
     } catch (...) {
-        host_error() = "unknown error";
+        set_host_error("unknown error");
         return EXPMC_RUNTIME_ERROR;
     }
 }

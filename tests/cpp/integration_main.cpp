@@ -32,7 +32,10 @@ static SplitMatrix make(std::uint64_t seed) {
     return split(generate(g));
 }
 
+#define STEP(x) std::printf("step %s\n", x)
+
 int main() {
+    std::setvbuf(stdout, nullptr, _IONBF, 0);
     PathParams p;
     p.beta = 0.05;
     p.n_steps = 32;
@@ -42,6 +45,7 @@ int main() {
     std::vector<double> v(m.n);
     for (std::size_t i = 0; i < m.n; ++i) v[i] = std::sin(0.37 * (double)i) + 0.1;
     const NodeId rows[] = {0, 1, 7, 123, 4567, 19999};
+    STEP("1. the drop-in");
     // 1. the drop-in call against the reference's own estimator
     for (NodeId i : rows) {
         const Estimate g = gpu::entry_estimate(m, v, i, p);
@@ -52,6 +56,7 @@ int main() {
                                                          r.std_error * r.std_error);
         if (!(std::fabs(z) < 5.0)) return fail("entry z", g.value, r.value);
     }
+    STEP("2. same errors");
     // 2. same errors as the reference
     try {
         gpu::entry_estimate(m, v, (NodeId)m.n, p);
@@ -59,6 +64,7 @@ int main() {
     } catch (const std::invalid_argument& e) {
         if (std::string(e.what()) != "entry index out of range") return fail("range message");
     }
+    STEP("3. a different ma");
     // 3. a different matrix at the same address (a seed sweep) is not served
     //    from the stale device copy
     const Estimate before = gpu::entry_estimate(m, v, 7, p);
@@ -73,6 +79,7 @@ int main() {
         if (!(std::fabs(z) < 5.0)) return fail("rebuilt-matrix z", after.value, r.value);
         if (before.value == after.value) return fail("stale device copy", before.value);
     }
+    STEP("4. concurrent cal");
     // 4. concurrent callers share one SplitMatrix: each gets its
     //    serial result
     std::vector<Estimate> serial;
@@ -85,10 +92,12 @@ int main() {
     for (std::size_t k = 0; k < std::size(rows); ++k)
         if (par[k].value != serial[k].value || par[k].total_jumps != serial[k].total_jumps)
             return fail("concurrent", par[k].value, serial[k].value);
+    STEP("5. the batched");
     // 5. the batched multi-device call equals the single-row calls
     const std::vector<Estimate> many = gpu::entries_estimate(m, v, rows, p, 1);
     for (std::size_t k = 0; k < std::size(rows); ++k)
         if (many[k].value != serial[k].value) return fail("batched", many[k].value);
+    STEP("6. Theorem-2");
     // 6. Theorem-2 estimators against the reference
     std::vector<double> w(m.n);
     for (std::size_t i = 0; i < m.n; ++i) w[i] = 1.0 + 0.5 * std::cos(0.11 * (double)i);
