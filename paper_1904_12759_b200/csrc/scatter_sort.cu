@@ -1,13 +1,19 @@
 // Deterministic per-end-state accumulation for the Theorem-2 estimators
-// (vector_estimate, proj/src/estimator.cpp:250 `local_values[out.end] += f`).
+// (vector_estimate, proj/src/estimator.cpp:250 `local_values[out.end] += f`)
+// and per-row sums of the large-W entry path.
 //
 // The walkers of a batch emit (end, f) records in a fixed order (walker /
 // jumper index); a stable radix sort by end keeps that order inside each end
-// state.  Every run is then summed in that order in fixed 32-record pieces
-// (pass A: pieces, runs inside one piece added at once; pass B: runs that
-// cross piece boundaries, pieces added in order) and added to values[end].
-// Each run is added by exactly one thread, so there are no atomics; batches
-// are applied in order, so the result is bitwise reproducible.  (CUB's
+// state.  Every run of equal keys is then summed by a fixed 32-ary tree:
+// level 0 sums each 32-record chunk's run pieces sequentially; a run that
+// lies inside one chunk is added to values[key] there, and each chunk hands
+// its first and last run pieces (0.0 when that run is already complete) to
+// the next level as two (key, piece) records — still sorted, pieces in chunk
+// order — and the level recurses until a level fits one chunk.  Each run is
+// completed, and added to values[key], by exactly one thread at one level,
+// so there are no atomics and the result is bitwise reproducible; batches
+// are applied in order.  Depth log_16(count): runs of any length (a hub end
+// state, one row of 2^30 walkers) cost the same as short ones.  (CUB's
 // ReduceByKey combines tile prefixes in a timing-dependent order, which is
 // not bitwise reproducible for doubles.)
 #include <stdexcept>
@@ -26,16 +32,17 @@ constexpr int kPieceThreads = 128;
 constexpr int kPad = kChunk + 1;  // smem row stride (bank-conflict-free chunk walks)
 constexpr size_t kPieceSmem = (size_t)kPieceThreads * kPad * (sizeof(uint32_t) + sizeof(double));
 
-// Pass A: thread k owns chunk [kC, kC + C) of the sorted records and sums
+// One level: thread k owns chunk [kC, kC + C) of the sorted records and sums
 // every run piece in it sequentially.  A run that starts and ends in the
-// chunk is added to values[] here; the piece of a run that started earlier
-// goes to head[k]; the piece of a run that starts here and continues past
-// the chunk goes to tail[k] (completed in pass B).  The block's records are
-// staged through shared memory with coalesced loads first.
+// chunk is added to values[] here.  The chunk's first run piece (when its run
+// started in an earlier chunk) and its last run piece (when its run goes on
+// past the chunk) become the next level's records 2k and 2k + 1, keyed by the
+// chunk's first and last keys (0.0 where there is no such piece).  The
+// block's records are staged through shared memory with coalesced loads.
 __global__ void __launch_bounds__(kPieceThreads)
-run_pieces_kernel(const uint32_t* __restrict__ keys, const double* __restrict__ f,
-                  uint64_t count, double* __restrict__ head, double* __restrict__ tail,
-                  double* __restrict__ values) {
+run_level_kernel(const uint32_t* __restrict__ keys, const double* __restrict__ f,
+                 uint64_t count, double* __restrict__ values, uint32_t* __restrict__ nkeys,
+                 double* __restrict__ nvals) {
     extern __shared__ double smem[];
     double* sf = smem;
     uint32_t* sk = reinterpret_cast<uint32_t*>(smem + kPieceThreads * kPad);
@@ -55,6 +62,7 @@ run_pieces_kernel(const uint32_t* __restrict__ keys, const double* __restrict__ 
     const uint32_t* ck = sk + threadIdx.x * kPad;
     const double* cf = sf + threadIdx.x * kPad;
     const bool last_chunk = lo + len == count;
+    double head = 0.0, tail = 0.0;
     uint32_t pos = 0;
     while (pos < len) {
         const uint32_t key = ck[pos];
@@ -63,32 +71,17 @@ run_pieces_kernel(const uint32_t* __restrict__ keys, const double* __restrict__ 
         uint32_t j = pos + 1;
         while (j < len && ck[j] == key) s = __dadd_rn(s, cf[j++]);
         const bool ends = j < len || last_chunk || keys[lo + len] != key;
-        if (!started) head[k] = s;
+        if (!started) head = s;       // (the run may also go on past the chunk)
         else if (ends) values[key] = __dadd_rn(values[key], s);
-        else tail[k] = s;
+        else tail = s;
         pos = j;
     }
-}
-
-// Pass B: thread k completes the run that starts in its chunk and crosses
-// its end: tail[k] + head[k+1] + head[k+2] + ... in chunk order.
-__global__ void run_spans_kernel(const uint32_t* __restrict__ keys, uint64_t count,
-                                 const double* __restrict__ head,
-                                 const double* __restrict__ tail, double* __restrict__ values) {
-    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    const uint64_t lo = k * kChunk, hi = lo + kChunk;
-    if (hi >= count) return;  // the last chunk has nothing past its end
-    const uint32_t key = keys[hi - 1];
-    if (keys[hi] != key) return;  // no run crosses the end of this chunk
-    // the crossing run started here unless it also covers this chunk's start
-    if (keys[lo] == key && (lo > 0 && keys[lo - 1] == key)) return;
-    double s = tail[k];
-    for (uint64_t c = k + 1; c * kChunk < count && keys[c * kChunk] == key; ++c) {
-        s = __dadd_rn(s, head[c]);
-        const uint64_t e = (c + 1) * kChunk;
-        if (e >= count || keys[e] != key) break;
+    if (nkeys) {
+        nkeys[2 * k] = ck[0];
+        nvals[2 * k] = head;
+        nkeys[2 * k + 1] = ck[len - 1];
+        nvals[2 * k + 1] = tail;
     }
-    values[key] = __dadd_rn(values[key], s);
 }
 
 int key_bits(uint64_t n) {
@@ -104,8 +97,7 @@ size_t scatter_sort_temp_bytes(uint64_t batch, uint64_t n) {
     cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                     (const double*)nullptr, (double*)nullptr, (int)batch, 0,
                                     key_bits(n));
-    const uint64_t chunks = (batch + kChunk - 1) / kChunk;
-    return a + 256 + 2 * chunks * sizeof(double) + 256;
+    return a + 256 + run_sums_temp_bytes(batch);
 }
 
 void scatter_sort_accumulate(uint32_t* end, double* f, uint32_t* end_sorted, double* f_sorted,
@@ -115,7 +107,7 @@ void scatter_sort_accumulate(uint32_t* end, double* f, uint32_t* end_sorted, dou
     size_t tb = 0;  // the sort's own share of temp (the piece buffers follow it)
     cub::DeviceRadixSort::SortPairs(nullptr, tb, end, end_sorted, f, f_sorted, (int)count, 0,
                                     key_bits(n));
-    if (tb + 512 + 2 * ((count + kChunk - 1) / kChunk) * sizeof(double) > temp_bytes)
+    if (((tb + 255) & ~(size_t)255) + run_sums_temp_bytes(count) > temp_bytes)
         throw std::runtime_error("scatter_sort: temp storage too small");
     cub::DeviceRadixSort::SortPairs(temp, tb, end, end_sorted, f, f_sorted, (int)count, 0,
                                     key_bits(n), s);
@@ -125,24 +117,45 @@ void scatter_sort_accumulate(uint32_t* end, double* f, uint32_t* end_sorted, dou
 }
 
 size_t run_sums_temp_bytes(uint64_t count) {
-    return 2 * ((count + kChunk - 1) / kChunk) * sizeof(double) + 256;
+    // two ping-pong levels of (u32 key, f64 piece) records, 2 per chunk
+    const uint64_t c1 = 2 * ((count + kChunk - 1) / kChunk);
+    return 2 * (c1 * (sizeof(uint32_t) + sizeof(double)) + 512) + 256;
 }
 
-// out[key] += sum of each run of equal keys (keys sorted), in record order.
+// out[key] += sum of each run of equal keys (keys sorted), in record order
+// grouped by the fixed 32-ary tree above.
 void run_sums_sorted(const uint32_t* keys, const double* vals, uint64_t count, void* temp,
                      size_t temp_bytes, double* out, cudaStream_t s) {
     if (count == 0) return;
-    const uint64_t chunks = (count + kChunk - 1) / kChunk;
-    if (2 * chunks * sizeof(double) > temp_bytes)
+    if (run_sums_temp_bytes(count) > temp_bytes)
         throw std::runtime_error("run_sums: temp storage too small");
-    double* head = static_cast<double*>(temp);
-    double* tail = head + chunks;
-    cudaFuncSetAttribute(run_pieces_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const uint64_t c1 = 2 * ((count + kChunk - 1) / kChunk);
+    const size_t region = ((c1 * (sizeof(uint32_t) + sizeof(double)) + 511) / 256) * 256;
+    unsigned char* t = static_cast<unsigned char*>(temp);
+    t = reinterpret_cast<unsigned char*>(((uintptr_t)t + 255) & ~(uintptr_t)255);
+    double* vbuf[2] = {reinterpret_cast<double*>(t), reinterpret_cast<double*>(t + region)};
+    uint32_t* kbuf[2] = {reinterpret_cast<uint32_t*>(vbuf[0] + c1),
+                         reinterpret_cast<uint32_t*>(vbuf[1] + c1)};
+    cudaFuncSetAttribute(run_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kPieceSmem);  // per device; cheap
-    run_pieces_kernel<<<(unsigned)((chunks + kPieceThreads - 1) / kPieceThreads), kPieceThreads,
-                        kPieceSmem, s>>>(keys, vals, count, head, tail, out);
-    run_spans_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, s>>>(keys, count, head, tail,
-                                                                      out);
+    const uint32_t* k = keys;
+    const double* v = vals;
+    uint64_t n = count;
+    for (int lvl = 0;; ++lvl) {
+        const uint64_t chunks = (n + kChunk - 1) / kChunk;
+        const unsigned grid = (unsigned)((chunks + kPieceThreads - 1) / kPieceThreads);
+        if (chunks == 1) {
+            run_level_kernel<<<grid, kPieceThreads, kPieceSmem, s>>>(k, v, n, out, nullptr,
+                                                                    nullptr);
+            break;
+        }
+        uint32_t* nk = kbuf[lvl & 1];
+        double* nv = vbuf[lvl & 1];
+        run_level_kernel<<<grid, kPieceThreads, kPieceSmem, s>>>(k, v, n, out, nk, nv);
+        k = nk;
+        v = nv;
+        n = 2 * chunks;
+    }
 }
 
 }  // namespace expmc_b200
