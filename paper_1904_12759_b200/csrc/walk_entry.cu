@@ -72,6 +72,15 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef ENTRY_UNCOND_LD
 #define ENTRY_UNCOND_LD 1 // issue the jump gather for every lane (no predicated moves behind it)
 #endif
+#ifndef ENTRY_KEEP_J
+#define ENTRY_KEEP_J 1 // keep the unused word of the gathered slot live (no register moves behind the gather)
+#endif
+#ifndef ENTRY_ROTATE
+#define ENTRY_ROTATE 1 // loop trip = jump, accumulate/admit, then sojourn + pop (gather consumed in the trip that issued it)
+#endif
+#ifndef ENTRY_LATE_COPY
+#define ENTRY_LATE_COPY 1 // gather into fresh registers, copied into the state at the consumer
+#endif
 #ifndef ENTRY_POP_MIN
 #define ENTRY_POP_MIN 2 // run the scheduler once this many lanes are idle
 #endif
@@ -175,6 +184,12 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     // the current state as the raw 32-byte Edge slot it was gathered from
     // ({j, off}, {deg_flags, inv_rate}, d, v)
     unsigned long long ea = 0, eb = 0, ec = 0, ed = 0;
+#if ENTRY_LATE_COPY
+    // the slot being gathered: fresh registers written only by the load, and
+    // copied into the state by pinned (volatile) moves at the consumer, so
+    // that no register move of loaded data sits behind the load itself
+    unsigned long long la = 0, lb = 0, lc = 0, ld = 0;
+#endif
 #define OFF ((uint32_t)(ea >> 32))
 #define DEGF ((uint32_t)eb)
 #define IR (__uint_as_float((uint32_t)(eb >> 32)))
@@ -197,6 +212,16 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, DCUR)) : S;
             q.v[pos] = VCUR;
             q.tk[tk_slot(pos)].x = jc;
+#if ENTRY_KEEP_J
+            // The landing row id (word 0 of the gathered slot) is not needed,
+            // and ptxas compacts the registers of a load with a dead word by
+            // moves placed right behind the load: the warp then waits for the
+            // gather before the accumulation / admission work instead of
+            // after it (24.7% of the stall samples sat on that move,
+            // profiles/r02).  A store of the word to the sink slot on this
+            // path keeps all eight registers in place.
+            q.tk[CAP].y = (uint32_t)ea;
+#endif
             act = false;
             fin = true;
         } else {
@@ -340,61 +365,8 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     };
 
     while (true) {
-        // ---- A: sojourn of every walker in flight
-        bool fin = false, jmp = false;
-        if (act) sojourn(neg_ln_u(ew), fin, jmp);
-        unsigned idle = __ballot_sync(FULL, !act);
-        // scheduler work only when enough lanes are free (batching pops
-        // amortises the scheduler over several walkers)
-        if (__popc(idle) < ENTRY_POP_MIN && idle != FULL) idle = 0;
-        if (idle) {
-            // ---- admit: sweep chunks while queued tickets cannot feed the
-            // idle lanes and a whole chunk's tickets fit in the ring
-            while (can_admit() && tail - head < (uint32_t)__popc(idle)) admit();
-            // ---- pop: idle lanes take tickets in order
-            const uint32_t avail = tail - head;
-            const uint32_t nidle = (uint32_t)__popc(idle);
-            const uint32_t take = avail < nidle ? avail : nidle;
-            const uint32_t rank = (uint32_t)__popc(idle & lt);
-            if (!act && rank < take) {
-                tk = head + rank;
-                const uint2 t2 = q.tk[tk_slot(tk & (CAP - 1))];
-                wl = t2.y & 0x1fffffffu;
-                const TaskRec& m = q.task[t2.y >> 29];
-                const uint4 r0 = *reinterpret_cast<const uint4*>(&m.rr);  // off, degf, ir, -
-                ea = (unsigned long long)r0.x << 32;
-                eb = r0.y | ((unsigned long long)r0.z << 32);
-                ec = (unsigned long long)__double_as_longlong(m.rr.d);
-                ed = (unsigned long long)__double_as_longlong(m.rr.v);
-                wi = m.i;
-                t = 0.0; S = 0.0; G = 0.0; jc = 0;
-                act = true;
-                // a jumper's first sojourn (R < λ) ends in a jump, so it joins
-                // this iteration's jump
-                sojourn(__uint_as_float(t2.x), fin, jmp);
-            }
-            head += take;
-#ifdef ENTRY_STATS
-            if (lane == 0) {
-                atomicAdd(p.stats + 1, (unsigned long long)nidle);
-                if (avail < nidle) {  // lanes left idle: why?
-                    atomicAdd(p.stats + 2, (unsigned long long)(nidle - avail));
-                    if (atask < ntask) atomicAdd(p.stats + 3, 1ull);  // ring full
-                }
-            }
-#endif
-        }
-#ifdef ENTRY_STATS
-        {
-            const unsigned jb = __ballot_sync(FULL, jmp);
-            const unsigned ab = __ballot_sync(FULL, act);
-            if (lane == 0) {
-                atomicAdd(p.stats + 0, 1ull);
-                atomicAdd(p.stats + 4, (unsigned long long)__popc(jb));
-                atomicAdd(p.stats + 5, (unsigned long long)__popc(ab));
-            }
-        }
-#endif
+#if ENTRY_ROTATE
+#define JMP act
         // ---- C: one jump for every walker whose sojourn did not end the path.
         // After the pop every walker still in flight must jump (jmp == act),
         // so the gather is issued unconditionally (idle lanes re-read slot 0
@@ -406,14 +378,18 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
 #if ENTRY_UNCOND_LD
         {
 #else
-        if (jmp) {
+        if (JMP) {
 #endif
             const U4 B = philox4x32_10(U4{jc, wl, wi, kTagEntry}, p.rk);
             const uint32_t off = OFF, degf = DEGF;
             uint32_t k = pick_index(B.y, B.w, degf & kDegMask);
-            if (jmp && (degf & kNonUniform) && B.z >= __ldg(thr + off + k))
+            if (JMP && (degf & kNonUniform) && B.z >= __ldg(thr + off + k))
                 k = __ldg(alias + off + k);
-            ld256(adj + (jmp ? off + k : 0u), ea, eb, ec, ed);
+#if ENTRY_LATE_COPY
+            ld256(adj + (JMP ? off + k : 0u), la, lb, lc, ld);
+#else
+            ld256(adj + (JMP ? off + k : 0u), ea, eb, ec, ed);
+#endif
             ew = B.x;
             ++jc;
         }
@@ -484,6 +460,232 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         }
         }
         if (tf == tw && !aopen && atask >= ntask) break;  // every task finalized
+        // ---- A: sojourn of every walker in flight
+        bool fin = false, jmp = false;
+#if ENTRY_LATE_COPY
+        if (act) {
+            asm volatile("mov.b64 %0, %4;\n\tmov.b64 %1, %5;\n\tmov.b64 %2, %6;\n\tmov.b64 %3, %7;"
+                         : "=l"(ea), "=l"(eb), "=l"(ec), "=l"(ed)
+                         : "l"(la), "l"(lb), "l"(lc), "l"(ld));
+            sojourn(neg_ln_u(ew), fin, jmp);
+        }
+#else
+        if (act) sojourn(neg_ln_u(ew), fin, jmp);
+#endif
+        unsigned idle = __ballot_sync(FULL, !act);
+        // scheduler work only when enough lanes are free (batching pops
+        // amortises the scheduler over several walkers)
+        if (__popc(idle) < ENTRY_POP_MIN && idle != FULL) idle = 0;
+        if (idle) {
+            // ---- admit: sweep chunks while queued tickets cannot feed the
+            // idle lanes and a whole chunk's tickets fit in the ring
+            while (can_admit() && tail - head < (uint32_t)__popc(idle)) admit();
+            // ---- pop: idle lanes take tickets in order
+            const uint32_t avail = tail - head;
+            const uint32_t nidle = (uint32_t)__popc(idle);
+            const uint32_t take = avail < nidle ? avail : nidle;
+            const uint32_t rank = (uint32_t)__popc(idle & lt);
+            if (!act && rank < take) {
+                tk = head + rank;
+                const uint2 t2 = q.tk[tk_slot(tk & (CAP - 1))];
+                wl = t2.y & 0x1fffffffu;
+                const TaskRec& m = q.task[t2.y >> 29];
+                const uint4 r0 = *reinterpret_cast<const uint4*>(&m.rr);  // off, degf, ir, -
+                ea = (unsigned long long)r0.x << 32;
+                eb = r0.y | ((unsigned long long)r0.z << 32);
+                ec = (unsigned long long)__double_as_longlong(m.rr.d);
+                ed = (unsigned long long)__double_as_longlong(m.rr.v);
+                wi = m.i;
+                t = 0.0; S = 0.0; G = 0.0; jc = 0;
+                act = true;
+                // a jumper's first sojourn (R < λ) ends in a jump, so it joins
+                // this iteration's jump
+                sojourn(__uint_as_float(t2.x), fin, jmp);
+            }
+            head += take;
+#ifdef ENTRY_STATS
+            if (lane == 0) {
+                atomicAdd(p.stats + 1, (unsigned long long)nidle);
+                if (avail < nidle) {  // lanes left idle: why?
+                    atomicAdd(p.stats + 2, (unsigned long long)(nidle - avail));
+                    if (atask < ntask) atomicAdd(p.stats + 3, 1ull);  // ring full
+                }
+            }
+#endif
+        }
+#ifdef ENTRY_STATS
+        {
+            const unsigned jb = __ballot_sync(FULL, jmp);
+            const unsigned ab = __ballot_sync(FULL, act);
+            if (lane == 0) {
+                atomicAdd(p.stats + 0, 1ull);
+                atomicAdd(p.stats + 4, (unsigned long long)__popc(jb));
+                atomicAdd(p.stats + 5, (unsigned long long)__popc(ab));
+            }
+        }
+#endif
+#undef JMP
+#else
+#define JMP jmp
+        // ---- A: sojourn of every walker in flight
+        bool fin = false, jmp = false;
+#if ENTRY_LATE_COPY
+        if (act) {
+            asm volatile("mov.b64 %0, %4;\n\tmov.b64 %1, %5;\n\tmov.b64 %2, %6;\n\tmov.b64 %3, %7;"
+                         : "=l"(ea), "=l"(eb), "=l"(ec), "=l"(ed)
+                         : "l"(la), "l"(lb), "l"(lc), "l"(ld));
+            sojourn(neg_ln_u(ew), fin, jmp);
+        }
+#else
+        if (act) sojourn(neg_ln_u(ew), fin, jmp);
+#endif
+        unsigned idle = __ballot_sync(FULL, !act);
+        // scheduler work only when enough lanes are free (batching pops
+        // amortises the scheduler over several walkers)
+        if (__popc(idle) < ENTRY_POP_MIN && idle != FULL) idle = 0;
+        if (idle) {
+            // ---- admit: sweep chunks while queued tickets cannot feed the
+            // idle lanes and a whole chunk's tickets fit in the ring
+            while (can_admit() && tail - head < (uint32_t)__popc(idle)) admit();
+            // ---- pop: idle lanes take tickets in order
+            const uint32_t avail = tail - head;
+            const uint32_t nidle = (uint32_t)__popc(idle);
+            const uint32_t take = avail < nidle ? avail : nidle;
+            const uint32_t rank = (uint32_t)__popc(idle & lt);
+            if (!act && rank < take) {
+                tk = head + rank;
+                const uint2 t2 = q.tk[tk_slot(tk & (CAP - 1))];
+                wl = t2.y & 0x1fffffffu;
+                const TaskRec& m = q.task[t2.y >> 29];
+                const uint4 r0 = *reinterpret_cast<const uint4*>(&m.rr);  // off, degf, ir, -
+                ea = (unsigned long long)r0.x << 32;
+                eb = r0.y | ((unsigned long long)r0.z << 32);
+                ec = (unsigned long long)__double_as_longlong(m.rr.d);
+                ed = (unsigned long long)__double_as_longlong(m.rr.v);
+                wi = m.i;
+                t = 0.0; S = 0.0; G = 0.0; jc = 0;
+                act = true;
+                // a jumper's first sojourn (R < λ) ends in a jump, so it joins
+                // this iteration's jump
+                sojourn(__uint_as_float(t2.x), fin, jmp);
+            }
+            head += take;
+#ifdef ENTRY_STATS
+            if (lane == 0) {
+                atomicAdd(p.stats + 1, (unsigned long long)nidle);
+                if (avail < nidle) {  // lanes left idle: why?
+                    atomicAdd(p.stats + 2, (unsigned long long)(nidle - avail));
+                    if (atask < ntask) atomicAdd(p.stats + 3, 1ull);  // ring full
+                }
+            }
+#endif
+        }
+#ifdef ENTRY_STATS
+        {
+            const unsigned jb = __ballot_sync(FULL, jmp);
+            const unsigned ab = __ballot_sync(FULL, act);
+            if (lane == 0) {
+                atomicAdd(p.stats + 0, 1ull);
+                atomicAdd(p.stats + 4, (unsigned long long)__popc(jb));
+                atomicAdd(p.stats + 5, (unsigned long long)__popc(ab));
+            }
+        }
+#endif
+        // ---- C: one jump for every walker whose sojourn did not end the path.
+        // After the pop every walker still in flight must jump (jmp == act),
+        // so the gather is issued unconditionally (idle lanes re-read slot 0
+        // and are re-initialised at their next pop): the 256-bit load then
+        // lands straight in the loop-carried registers, with no predicated
+        // register moves right behind it to stall on, and its latency hides
+        // behind the accumulation / admission work below until the next
+        // iteration's sojourn reads the new state.
+#if ENTRY_UNCOND_LD
+        {
+#else
+        if (JMP) {
+#endif
+            const U4 B = philox4x32_10(U4{jc, wl, wi, kTagEntry}, p.rk);
+            const uint32_t off = OFF, degf = DEGF;
+            uint32_t k = pick_index(B.y, B.w, degf & kDegMask);
+            if (JMP && (degf & kNonUniform) && B.z >= __ldg(thr + off + k))
+                k = __ldg(alias + off + k);
+#if ENTRY_LATE_COPY
+            ld256(adj + (JMP ? off + k : 0u), la, lb, lc, ld);
+#else
+            ld256(adj + (JMP ? off + k : 0u), ea, eb, ec, ed);
+#endif
+            ew = B.x;
+            ++jc;
+        }
+        // ---- accumulate finished tickets in batches of 32 (lane = ticket -
+        // tstart mod 32) and finalize completed tasks, oldest first.  Tickets
+        // [xc, xc + rdy) are popped and finished: the oldest ticket still
+        // walking (or the first not popped) bounds them.
+        const uint32_t minoff = __reduce_min_sync(FULL, act ? tk - xc : ~0u);
+        uint32_t rdy = head - xc < minoff ? head - xc : minoff;
+        if (rdy >= 32u || (ocl && rdy >= oend - xc)) {
+        __syncwarp();
+        while (tf != tw) {
+            const TaskRec& m = q.task[tf & (RT - 1)];
+            // ready tickets of this task (offsets from xc)
+            const uint32_t lim = ocl && oend - xc < rdy ? oend - xc : rdy;
+            uint32_t nb;
+            if (lim >= 32u) {
+                nb = 32u;                     // a full batch
+            } else if (ocl && lim == oend - xc) {
+                nb = lim;                     // the closed task's last (partial) batch
+            } else {
+                break;                        // wait for more tickets
+            }
+            if (nb) {
+                if ((uint32_t)lane < nb) {
+                    const uint32_t pos = (xc + lane) & (CAP - 1);
+                    const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], m.corr));
+                    const double dv = __dsub_rn(__dmul_rn(exp_det(x), q.v[pos]), m.K);
+                    s1 = __dadd_rn(s1, dv);
+                    s2 = __fma_rn(dv, dv, s2);
+                    jsum += q.tk[tk_slot(pos)].x;
+                }
+                xc += nb;
+                rdy -= nb;
+            }
+            if (!ocl || xc != oend) continue;
+            // task complete: butterfly, never-jumpers, output
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                s1 = __dadd_rn(s1, __shfl_xor_sync(FULL, s1, o));
+                s2 = __dadd_rn(s2, __shfl_xor_sync(FULL, s2, o));
+                jsum += __shfl_xor_sync(FULL, jsum, o);
+            }
+            if (lane == 0) {
+                // never-jumpers score f0: deviation f0 - K each (0 when K = f0)
+                const double f0 = m.f0, K = m.K;
+                const uint32_t n0 = m.n0;
+                const double c = __dsub_rn(f0, K);
+                if (n0 != 0 && c != 0.0) {
+                    s1 = __fma_rn((double)n0, c, s1);
+                    s2 = __fma_rn((double)n0, __dmul_rn(c, c), s2);
+                }
+                // the divisions and sqrt of the estimate run in the
+                // row-parallel combine pass, not on one lane here
+                partial[m.task] = make_double4(s1, s2, __longlong_as_double((long long)jsum), K);
+            }
+            s1 = 0.0;
+            s2 = 0.0;
+            jsum = 0;
+            ++tf;
+            __syncwarp();
+            ocl = false;
+            if (tf != tw) {
+                const uint2 e = *reinterpret_cast<const uint2*>(&q.task[tf & (RT - 1)].tend);
+                ocl = e.y != 0u;
+                oend = e.x;
+            }
+        }
+        }
+        if (tf == tw && !aopen && atask >= ntask) break;  // every task finalized
+#undef JMP
+#endif
     }
 }
 #undef OFF
@@ -491,6 +693,8 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
 #undef IR
 #undef DCUR
 #undef VCUR
+
+#include "walk_entry_short.cuh"
 
 // Combine the parts of each row in index order (same tree as the contract:
 // part 0, then += part 1, ...) and form the estimate: mean K + Σdev / W,
@@ -536,9 +740,13 @@ struct LaunchCfg {
     int nsm, pad;
 };
 
-template <int WPR, int BL>
-const LaunchCfg& launch_cfg() {
-    static const LaunchCfg lc = [] {
+using EntryKernel = void (*)(const RowRec*, const double*, const Edge*, const uint32_t*,
+                             const uint32_t*, const uint32_t*, uint64_t, FastParams, double4*,
+                             unsigned int*);
+
+template <EntryKernel KERN, int BL>
+const LaunchCfg& launch_cfg(const char* name) {
+    static const LaunchCfg lc = [name] {
         int nsm = 0, pad = 0;
         int dev = 0, smem_sm = 0;
         cudaFuncAttributes fa;
@@ -546,7 +754,7 @@ const LaunchCfg& launch_cfg() {
         if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
             nsm = 148;
         int pct = -1;
-        if (ENTRY_CARVE && cudaFuncGetAttributes(&fa, entry_walk_kernel<WPR, BL>) == cudaSuccess &&
+        if (ENTRY_CARVE && cudaFuncGetAttributes(&fa, KERN) == cudaSuccess &&
             cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) ==
                 cudaSuccess &&
             smem_sm > 0) {
@@ -562,32 +770,29 @@ const LaunchCfg& launch_cfg() {
             const long tmin = smem_sm / (BL + 1) - kReserve + 1;  // BL+1 blocks must not fit
             const long tmax = cap / BL - kReserve;                 // BL blocks must fit in cap
             if (tmin <= tmax) pad = (int)(tmin > st ? tmin - st : 0);
-            if (pad) cudaFuncSetAttribute(entry_walk_kernel<WPR, BL>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+            if (pad) cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
             // the driver rounds the percentage UP to a supported capacity
             pct = (int)floor(100.0 * cap / smem_sm);
-            cudaFuncSetAttribute(entry_walk_kernel<WPR, BL>,
-                                 cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+            cudaFuncSetAttribute(KERN, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
         }
         int resident = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, entry_walk_kernel<WPR, BL>, 128,
-                                                      pad);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, KERN, 128, pad);
         cudaGetLastError();
         if (getenv("EXPMC_DEBUG"))
             fprintf(stderr,
-                    "entry_walk_kernel<%d,%d>: %d SMs, occupancy %d blocks/SM, pad %d B, "
-                    "carveout %d%%\n",
-                    WPR, BL, nsm, resident, pad, pct);
+                    "%s<BL=%d>: %d SMs, occupancy %d blocks/SM, pad %d B, carveout %d%%\n", name,
+                    BL, nsm, resident, pad, pct);
         return LaunchCfg{nsm, pad};
     }();
     return lc;
 }
 
-template <int WPR, int BL>
-int launch_t(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const FastParams& p,
-             double* value, double* se, uint64_t* jumps, double4* partial, cudaStream_t s) {
+template <int WPR, EntryKernel KERN, int BL>
+int launch_t(const char* name, const DevSplit& m, const uint32_t* rows, uint64_t nrows,
+             const FastParams& p, double* value, double* se, uint64_t* jumps, double4* partial,
+             cudaStream_t s) {
     // Grid = one wave of resident blocks (the kernel strides over tasks).
-    const LaunchCfg& lc = launch_cfg<WPR, BL>();
+    const LaunchCfg& lc = launch_cfg<KERN, BL>(name);
     const int nsm = lc.nsm, pad = lc.pad;
     const uint64_t warps = nrows * WPR;
     const uint64_t blocks = (warps + 3) / 4;
@@ -597,31 +802,44 @@ int launch_t(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const Fast
 #if ENTRY_DYNAMIC
     cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s);
 #endif
-    entry_walk_kernel<WPR, BL><<<grid, 128, pad, s>>>(m.rec, m.rate, m.adj, m.alias_thr,
-                                                    m.alias_idx, rows, nrows, p, partial, ctr);
+    KERN<<<grid, 128, pad, s>>>(m.rec, m.rate, m.adj, m.alias_thr, m.alias_idx, rows, nrows, p,
+                                partial, ctr);
     combine_parts_kernel<WPR><<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(
         partial, nrows, p.W, value, se, jumps);
     return 2;
 }
 
-// Two launch shapes, chosen by the mean walk length (jumps of a walker
-// started at a random row); neither changes a result bit.
-//  * short walks (< ENTRY_SHORT_WALK jumps): 8 resident blocks per SM (32
-//    warps, ~38 KB of L1 left) — the kernel is issue/latency-bound on
-//    scheduling and arithmetic (config 5: 48.9 ms vs 51.1 ms at 7 blocks);
-//  * long walks: 7 blocks (28 warps, ~60 KB of L1 for the outstanding misses
-//    of the dependent gather chains; config 4: 2.95 s vs 4.59 s at 8).
-// Measured, profiles/r02/README.md.  (A Philox / Exp(1) lookahead for long
-// walks, off the gather-to-gather path, measured slower on config 4:
-// 3.25 s.)
+// Launch shapes, chosen by the mean walk length (jumps of a walker started at
+// a random row); none changes a result bit.
+//  * short walks (< ENTRY_SHORT_K3P jumps): the pipelined K3P kernel
+//    (walk_entry_short.cuh), EPIPE_BL blocks per SM;
+//  * medium (< ENTRY_SHORT_WALK jumps): entry_walk_kernel with 8 resident
+//    blocks per SM (32 warps, ~38 KB of L1 left);
+//  * long walks: entry_walk_kernel with 7 blocks (28 warps, ~60 KB of L1 for
+//    the outstanding misses of the dependent gather chains; config 4: 2.95 s
+//    vs 4.59 s at 8).
+// Measured, profiles/r02/README.md.  EXPMC_ENTRY_SHAPE (A/B and tests only):
+// 0 = 8 blocks, 1 = 7 blocks, 3 = K3P.
+#ifndef ENTRY_SHORT_K3P
+#define ENTRY_SHORT_K3P 2.0
+#endif
 template <int WPR>
 int launch_w(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const FastParams& p,
              double* value, double* se, uint64_t* jumps, double4* partial, cudaStream_t s) {
     const double walk = p.beta * m.mean_rate;
-    bool shortw = walk < ENTRY_SHORT_WALK;
-    if (const char* e = getenv("EXPMC_ENTRY_SHAPE")) shortw = atoi(e) == 0;  // A/B only
-    return shortw ? launch_t<WPR, 8>(m, rows, nrows, p, value, se, jumps, partial, s)
-                  : launch_t<WPR, 7>(m, rows, nrows, p, value, se, jumps, partial, s);
+    int shape = walk < ENTRY_SHORT_K3P ? 3 : (walk < ENTRY_SHORT_WALK ? 0 : 1);
+    if (const char* e = getenv("EXPMC_ENTRY_SHAPE")) shape = atoi(e);  // A/B only
+    switch (shape) {
+        case 3:
+            return launch_t<WPR, entry_pipe_kernel<WPR, EPIPE_BL>, EPIPE_BL>(
+                "entry_pipe_kernel", m, rows, nrows, p, value, se, jumps, partial, s);
+        case 0:
+            return launch_t<WPR, entry_walk_kernel<WPR, 8>, 8>("entry_walk_kernel", m, rows, nrows,
+                                                               p, value, se, jumps, partial, s);
+        default:
+            return launch_t<WPR, entry_walk_kernel<WPR, 7>, 7>("entry_walk_kernel", m, rows, nrows,
+                                                               p, value, se, jumps, partial, s);
+    }
 }
 
 }  // namespace
