@@ -212,7 +212,8 @@ __device__ const double2 kExpTab[32] = {
     {0x1.ea4afa2a490dap+0, -0x1.e9c23179c2893p-54},
     {0x1.f50765b6e4540p+0, 0x1.9d3e12dd8a18bp-54}};
 
-__device__ __forceinline__ double exp_det(double x) {
+// `tab`: kExpTab or a shared-memory copy of it (same values, same result).
+__device__ __forceinline__ double exp_det_tab(double x, const double2* __restrict__ tab, bool tab_global) {
     x = x > 710.0 ? 710.0 : x;
     x = x < -746.0 ? -746.0 : x;
     // n = rint(x 32/ln2) by the 1.5 2^52 shifter (round-to-nearest-even, as
@@ -230,13 +231,15 @@ __device__ __forceinline__ double exp_det(double x) {
     p = __fma_rn(p, r, 1.0);
     p = __dmul_rn(p, r);  // e^r - 1
     const int ni = (int)__double2loint(sh);
-    const double2 t = __ldg(&kExpTab[ni & 31]);
+    const double2 t = tab_global ? __ldg(&tab[ni & 31]) : tab[ni & 31];
     const double y = __dadd_rn(t.x, __fma_rn(t.x, p, t.y));
     const int k = ni >> 5;
     const int k1 = k >> 1;
     return __dmul_rn(__dmul_rn(y, __longlong_as_double((long long)(k1 + 1023) << 52)),
                      __longlong_as_double((long long)(k - k1 + 1023) << 52));
 }
+
+__device__ __forceinline__ double exp_det(double x) { return exp_det_tab(x, kExpTab, true); }
 
 // floor(x * n / 2^64) for a 64-bit uniform x: unbiased to n / 2^64.
 __device__ __forceinline__ uint32_t pick_index(uint32_t hi, uint32_t lo,

@@ -81,6 +81,15 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef ENTRY_LATE_COPY
 #define ENTRY_LATE_COPY 1 // gather into fresh registers, copied into the state at the consumer
 #endif
+#ifndef ENTRY_TAB_SHARED
+#define ENTRY_TAB_SHARED 1 // exp table in shared memory (8-block shape)
+#endif
+#ifndef ENTRY_AHEAD
+#define ENTRY_AHEAD 0 // (measured slower: cfg5 +4.8%, cfg4 +2.6%) claim tasks one ahead: row index loaded and record prefetched a task early
+#endif
+#ifndef ENTRY_EARLY_ADMIT
+#define ENTRY_EARLY_ADMIT 0 // (measured slower: cfg5 +5%, cfg2 +20%) rotated loop: admit before the sojourn while fewer tickets are queued (0: off)
+#endif
 #ifndef ENTRY_POP_MIN
 #define ENTRY_POP_MIN 2 // run the scheduler once this many lanes are idle
 #endif
@@ -158,6 +167,16 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     __shared__ WarpState<RT, CAP> states[4];
+    // exp_det's 2^(j/32) table: a shared-memory copy for the 8-block shape
+    // (the accumulation batches waited on its L1 lookups: 6.6% of the stall
+    // samples).  The 7-block shape keeps the L1 table: 512 B more per block
+    // would not fit its 196 KB carveout.
+    constexpr bool kTabShared = ENTRY_TAB_SHARED && BL >= 8;
+    __shared__ double2 s_tab[kTabShared ? 32 : 1];
+    if (kTabShared) {
+        if (threadIdx.x < 32) s_tab[threadIdx.x] = kExpTab[threadIdx.x];
+        __syncthreads();
+    }
     WarpState<RT, CAP>& q = states[warp];
     const uint32_t ntask = (uint32_t)(nrows * WPR);
     const uint32_t tstride = gridDim.x * 4u;
@@ -242,16 +261,48 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         if (lane == 0) t = tstride + atomicAdd(task_ctr, 1u);
         return __shfl_sync(FULL, t, 0);
 #else
-        return atask + tstride;
+        return anext + tstride;
 #endif
     };
+#if ENTRY_AHEAD
+    // Tasks are claimed one ahead: `anext` with its row index `inext` loaded
+    // when the previous task was claimed (the load lands during a whole
+    // task), and the row's record and rate prefetched into L2 when it becomes
+    // `atask` — open_task then finds them instead of waiting for two
+    // dependent DRAM round trips (rows[] -> rec[], rate[]).
+    auto load_row = [&](uint32_t t) -> uint32_t { return t < ntask ? __ldg(rows + t / WPR) : 0u; };
+    uint32_t irow = load_row(atask);
+    uint32_t anext = atask;
+    anext = next_task();
+    uint32_t inext = load_row(anext);
+    auto advance_task = [&] {
+        atask = anext;
+        irow = inext;
+        if (atask < ntask) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(rec + irow));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(rate + irow));
+        }
+        anext = next_task();
+        inext = load_row(anext);
+    };
+#else
+    uint32_t anext = atask;
+    auto advance_task = [&] {
+        anext = atask;
+        atask = next_task();
+    };
+#endif
 
     // Open task `atask` in slot tw: row constants computed by two lanes in
     // parallel (lane 0: e^{-λ}, lane 1: e^{β d}).  Part w of a row owns the
     // walkers [⌊wW/WPR⌋, ⌊(w+1)W/WPR⌋).
     auto open_task = [&] {
         const int sl = (int)(tw & (RT - 1));
+#if ENTRY_AHEAD
+        const uint32_t i = irow;
+#else
         const uint32_t i = rows[atask / WPR];
+#endif
         const RowRec ri = load_rec(rec, i);
         const double lam = __dmul_rn(__ldg(rate + i), p.beta);
         const double ex = exp_det(lane == 0 ? -lam : __dmul_rn(p.beta, ri.d));
@@ -285,7 +336,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         around = 0;
         atstart = tail;
         if (dead) {
-            atask = next_task();
+            advance_task();
         } else {
             aopen = true;
         }
@@ -359,7 +410,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 oend = tail;
             }
             aopen = false;
-            atask = next_task();
+            advance_task();
         }
         __syncwarp();
     };
@@ -417,7 +468,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 if ((uint32_t)lane < nb) {
                     const uint32_t pos = (xc + lane) & (CAP - 1);
                     const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], m.corr));
-                    const double dv = __dsub_rn(__dmul_rn(exp_det(x), q.v[pos]), m.K);
+                    const double dv = __dsub_rn(
+                        __dmul_rn(kTabShared ? exp_det_tab(x, s_tab, false) : exp_det(x), q.v[pos]),
+                        m.K);
                     s1 = __dadd_rn(s1, dv);
                     s2 = __fma_rn(dv, dv, s2);
                     jsum += q.tk[tk_slot(pos)].x;
@@ -460,6 +513,11 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         }
         }
         if (tf == tw && !aopen && atask >= ntask) break;  // every task finalized
+#if ENTRY_EARLY_ADMIT
+        // gap rounds ahead of need (fewer than a warp's worth of tickets
+        // queued), while this trip's gather is still in flight
+        while (can_admit() && tail - head < (uint32_t)ENTRY_EARLY_ADMIT) admit();
+#endif
         // ---- A: sojourn of every walker in flight
         bool fin = false, jmp = false;
 #if ENTRY_LATE_COPY
@@ -641,7 +699,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 if ((uint32_t)lane < nb) {
                     const uint32_t pos = (xc + lane) & (CAP - 1);
                     const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], m.corr));
-                    const double dv = __dsub_rn(__dmul_rn(exp_det(x), q.v[pos]), m.K);
+                    const double dv = __dsub_rn(
+                        __dmul_rn(kTabShared ? exp_det_tab(x, s_tab, false) : exp_det(x), q.v[pos]),
+                        m.K);
                     s1 = __dadd_rn(s1, dv);
                     s2 = __fma_rn(dv, dv, s2);
                     jsum += q.tk[tk_slot(pos)].x;
