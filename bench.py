@@ -241,13 +241,34 @@ def cpu_reference_rate(matrix, v, rows_all, walkers, n_steps, beta, seed, target
     _, _, j1 = matrix.entries(v, first, beta, n_steps, 1, 1, seed, workers=1, threads=cores)
     setup_s = time.perf_counter() - t
     s0, j0, r0 = out[0]
-    path_s = max(s0 - setup_s, 1e-9)
+    # Path-only rate by differencing: the same few rows with samples = 1
+    # (setup only) and with samples = F W, F raised until the walkers cost at
+    # least half the setup — on config 5 the W = 1e3 walkers of a row are
+    # ~0.01% of its call, far below the timing noise of (total - setup).
+    # (strided: the sorted sample starts with the low-index hub rows of BA graphs)
+    small = first[:: max(1, len(first) // (4 * cores))][: 4 * cores]
+    t = time.perf_counter()
+    matrix.entries(v, small, beta, n_steps, 1, 1, seed, workers=1, threads=cores)
+    t_lo = time.perf_counter() - t
+    F, t_hi, j_hi = 1, None, 0
+    for F in (16, 256, 4096, 65536):
+        t = time.perf_counter()
+        _, _, jh = matrix.entries(v, small, beta, n_steps, walkers * F, 1, seed, workers=1,
+                                  threads=cores)
+        t_hi, j_hi = time.perf_counter() - t, int(jh.sum())
+        if t_hi - t_lo >= 0.5 * t_lo or t_hi > 0.5 * target_s:
+            break
+    path_s = t_hi - t_lo
+    ok = path_s > 0.2 * t_hi and j_hi > 0
     split = {"setup_per_call_s": setup_s * cores / r0,
-             "setup_share": setup_s / s0,
-             "path_only_value": j0 / path_s,
-             "path_only_entries_per_s": r0 / path_s,
+             "setup_share": min(1.0, setup_s / s0),
+             "path_only_value": j_hi / path_s if ok else None,
+             "path_only_entries_per_s": (len(small) * F / path_s) if ok else None,
              "setup_how": f"same {r0} rows re-run with samples=1 (node_factors O(n) + "
-                          f"thread pool per call), row-parallel on {cores} threads"}
+                          f"thread pool per call), row-parallel on {cores} threads",
+             "path_only_how": f"{len(small)} rows at samples = {F} x W minus the same rows at "
+                              f"samples = 1 ({t_hi:.2f} s - {t_lo:.2f} s); entries/s counts "
+                              f"W-walker entries"}
     return out, cores, split
 
 

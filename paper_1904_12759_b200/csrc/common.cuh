@@ -276,6 +276,29 @@ __device__ __forceinline__ void ld256(const void* p, unsigned long long& a, unsi
                  : "l"(p));
 }
 
+// The walkers' random Edge gathers: same load with an L1 policy
+// (ENTRY_LD_HINT 1: L1::no_allocate, 2: L1::evict_first, 0: none).  The
+// gathered sectors are never reused from L1, and without an allocation per
+// gather the number of gathers in flight is no longer capped by the L1 lines
+// left beside the shared-memory carveout: config 4 at 8 blocks/SM (28 KB of
+// L1) 4.59 s -> 2.72 s, config 5 45.1 -> 44.1 ms (profiles/r02/README.md).
+#ifndef ENTRY_LD_HINT
+#define ENTRY_LD_HINT 1
+#endif
+__device__ __forceinline__ void ld256_gather(const void* p, unsigned long long& a,
+                                             unsigned long long& b, unsigned long long& c,
+                                             unsigned long long& d) {
+#if ENTRY_LD_HINT == 1
+    asm("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+#elif ENTRY_LD_HINT == 2
+    asm("ld.global.nc.L1::evict_first.v4.u64 {%0,%1,%2,%3}, [%4];"
+#else
+    asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+#endif
+        : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+        : "l"(p));
+}
+
 __device__ __forceinline__ Edge load_edge(const Edge* __restrict__ adj, uint32_t k) {
     unsigned long long a, b, c, d;
     ld256(adj + k, a, b, c, d);

@@ -51,9 +51,6 @@ namespace {
 constexpr int kRound = 128;  // gaps per warp round (4 per lane): at most kRound tickets
 constexpr unsigned FULL = 0xffffffffu;
 
-#ifndef ENTRY_SHORT_WALK
-#define ENTRY_SHORT_WALK 8.0 // mean jumps per walker below which 8 blocks/SM run (else 7)
-#endif
 #ifndef ENTRY_TASKS
 #define ENTRY_TASKS 8   // tasks in flight per warp (power of 2, <= 8: slot in 3 ticket bits)
 #endif
@@ -89,6 +86,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #endif
 #ifndef ENTRY_EARLY_ADMIT
 #define ENTRY_EARLY_ADMIT 0 // (measured slower: cfg5 +5%, cfg2 +20%) rotated loop: admit before the sojourn while fewer tickets are queued (0: off)
+#endif
+#ifndef ENTRY_LOOKAHEAD
+#define ENTRY_LOOKAHEAD 0 // (measured: cfg4 +1%, cfg1 +27%) 7-block (long-walk) shape: Philox block of the next jump drawn a trip ahead
 #endif
 #ifndef ENTRY_POP_MIN
 #define ENTRY_POP_MIN 2 // run the scheduler once this many lanes are idle
@@ -209,6 +209,11 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     // that no register move of loaded data sits behind the load itself
     unsigned long long la = 0, lb = 0, lc = 0, ld = 0;
 #endif
+    // lookahead (long-walk shape): the next jump's Philox block, whether the
+    // lane has one, and whether it jumped in this trip
+    constexpr bool kLookahead = ENTRY_LOOKAHEAD && ENTRY_ROTATE && ENTRY_LATE_COPY && BL <= 7;
+    uint32_t nbx = 0, nby = 0, nbz = 0, nbw = 0;
+    bool ready = false, go = false;
 #define OFF ((uint32_t)(ea >> 32))
 #define DEGF ((uint32_t)eb)
 #define IR (__uint_as_float((uint32_t)(eb >> 32)))
@@ -431,18 +436,45 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
 #else
         if (JMP) {
 #endif
+#if ENTRY_LOOKAHEAD
+            // Long-walk shape: the Philox block of a jump is drawn one trip
+            // ahead, off the gather -> sojourn -> jump chain (it depends on
+            // the jump count, not on the gathered state), and computed while
+            // this trip's gather is in flight.  A popped walker waits one
+            // trip for its first block (1 trip in ~β·rate).
+            if (kLookahead) {
+                go = act && ready;
+                const uint32_t off = OFF, degf = DEGF;
+                uint32_t k = pick_index(nby, nbw, degf & kDegMask);
+                if (go && (degf & kNonUniform) && nbz >= __ldg(thr + off + k))
+                    k = __ldg(alias + off + k);
+                ld256_gather(adj + (go ? off + k : 0u), la, lb, lc, ld);
+                if (go) {
+                    ew = nbx;
+                    ++jc;
+                }
+                const U4 B = philox4x32_10(U4{jc, wl, wi, kTagEntry}, p.rk);
+                nbx = B.x;
+                nby = B.y;
+                nbz = B.z;
+                nbw = B.w;
+                ready = act;
+            } else
+#endif
+            {
             const U4 B = philox4x32_10(U4{jc, wl, wi, kTagEntry}, p.rk);
             const uint32_t off = OFF, degf = DEGF;
             uint32_t k = pick_index(B.y, B.w, degf & kDegMask);
             if (JMP && (degf & kNonUniform) && B.z >= __ldg(thr + off + k))
                 k = __ldg(alias + off + k);
 #if ENTRY_LATE_COPY
-            ld256(adj + (JMP ? off + k : 0u), la, lb, lc, ld);
+            ld256_gather(adj + (JMP ? off + k : 0u), la, lb, lc, ld);
 #else
             ld256(adj + (JMP ? off + k : 0u), ea, eb, ec, ed);
 #endif
             ew = B.x;
             ++jc;
+            }
         }
         // ---- accumulate finished tickets in batches of 32 (lane = ticket -
         // tstart mod 32) and finalize completed tasks, oldest first.  Tickets
@@ -521,7 +553,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         // ---- A: sojourn of every walker in flight
         bool fin = false, jmp = false;
 #if ENTRY_LATE_COPY
-        if (act) {
+        if (kLookahead ? go : act) {
             asm volatile("mov.b64 %0, %4;\n\tmov.b64 %1, %5;\n\tmov.b64 %2, %6;\n\tmov.b64 %3, %7;"
                          : "=l"(ea), "=l"(eb), "=l"(ec), "=l"(ed)
                          : "l"(la), "l"(lb), "l"(lc), "l"(ld));
@@ -556,6 +588,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 wi = m.i;
                 t = 0.0; S = 0.0; G = 0.0; jc = 0;
                 act = true;
+                ready = false;
                 // a jumper's first sojourn (R < λ) ends in a jump, so it joins
                 // this iteration's jump
                 sojourn(__uint_as_float(t2.x), fin, jmp);
@@ -668,7 +701,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             if (JMP && (degf & kNonUniform) && B.z >= __ldg(thr + off + k))
                 k = __ldg(alias + off + k);
 #if ENTRY_LATE_COPY
-            ld256(adj + (JMP ? off + k : 0u), la, lb, lc, ld);
+            ld256_gather(adj + (JMP ? off + k : 0u), la, lb, lc, ld);
 #else
             ld256(adj + (JMP ? off + k : 0u), ea, eb, ec, ed);
 #endif
@@ -869,26 +902,20 @@ int launch_t(const char* name, const DevSplit& m, const uint32_t* rows, uint64_t
     return 2;
 }
 
-// Launch shapes, chosen by the mean walk length (jumps of a walker started at
-// a random row); none changes a result bit.
-//  * short walks (< ENTRY_SHORT_K3P jumps): the pipelined K3P kernel
-//    (walk_entry_short.cuh), EPIPE_BL blocks per SM;
-//  * medium (< ENTRY_SHORT_WALK jumps): entry_walk_kernel with 8 resident
-//    blocks per SM (32 warps, ~38 KB of L1 left);
-//  * long walks: entry_walk_kernel with 7 blocks (28 warps, ~60 KB of L1 for
-//    the outstanding misses of the dependent gather chains; config 4: 2.95 s
-//    vs 4.59 s at 8).
-// Measured, profiles/r02/README.md.  EXPMC_ENTRY_SHAPE (A/B and tests only):
-// 0 = 8 blocks, 1 = 7 blocks, 3 = K3P.
-#ifndef ENTRY_SHORT_K3P
-#define ENTRY_SHORT_K3P 2.0
-#endif
+// Launch shapes; none changes a result bit.  With the gathers marked
+// L1::no_allocate (common.cuh ld256_gather) the 8-block shape is the fastest
+// on every configuration (config 4: 2.72 s, against 2.79 s at 7 blocks), so
+// it is the only production shape.  EXPMC_ENTRY_SHAPE (A/B and tests only):
+// 0 = entry_walk_kernel, 8 blocks/SM (32 warps); 1 = 7 blocks (28 warps, 60 KB
+// of L1 — needed for long walks before the no-allocate gathers: 2.81 s vs
+// 4.59 s on config 4); 3 = the pipelined two-set entry_pipe_kernel
+// (walk_entry_short.cuh: bit-identical results, measured slower).
+// Measured, profiles/r02/README.md.
 template <int WPR>
 int launch_w(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const FastParams& p,
              double* value, double* se, uint64_t* jumps, double4* partial, cudaStream_t s) {
-    const double walk = p.beta * m.mean_rate;
-    int shape = walk < ENTRY_SHORT_K3P ? 3 : (walk < ENTRY_SHORT_WALK ? 0 : 1);
-    if (const char* e = getenv("EXPMC_ENTRY_SHAPE")) shape = atoi(e);  // A/B only
+    int shape = 0;
+    if (const char* e = getenv("EXPMC_ENTRY_SHAPE")) shape = atoi(e);  // A/B and tests only
     switch (shape) {
         case 3:
             return launch_t<WPR, entry_pipe_kernel<WPR, EPIPE_BL>, EPIPE_BL>(
@@ -896,6 +923,14 @@ int launch_w(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const Fast
         case 0:
             return launch_t<WPR, entry_walk_kernel<WPR, 8>, 8>("entry_walk_kernel", m, rows, nrows,
                                                                p, value, se, jumps, partial, s);
+#ifdef EXPMC_EXPERIMENTS
+        case 5:
+            return launch_t<WPR, entry_walk_kernel<WPR, 5>, 5>("entry_walk_kernel", m, rows, nrows,
+                                                               p, value, se, jumps, partial, s);
+        case 6:
+            return launch_t<WPR, entry_walk_kernel<WPR, 6>, 6>("entry_walk_kernel", m, rows, nrows,
+                                                               p, value, se, jumps, partial, s);
+#endif
         default:
             return launch_t<WPR, entry_walk_kernel<WPR, 7>, 7>("entry_walk_kernel", m, rows, nrows,
                                                                p, value, se, jumps, partial, s);

@@ -329,7 +329,7 @@ entry_pipe_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             if (s.act && (s.degf & kNonUniform) && B.z >= __ldg(thr + s.off + k))
                 k = __ldg(alias + s.off + k);
 #if EPIPE_REGS
-            ld256(adj + (s.act ? s.off + k : 0u), s.ea, s.eb, s.ec, s.ed);
+            ld256_gather(adj + (s.act ? s.off + k : 0u), s.ea, s.eb, s.ec, s.ed);
 #else
             const char* src = reinterpret_cast<const char*>(adj + (s.act ? s.off + k : 0u));
             const uint32_t nb = s.act ? 16u : 0u;

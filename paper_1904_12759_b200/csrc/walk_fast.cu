@@ -35,8 +35,17 @@ gather_ceiling_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ a
             h ^= h << 13; h ^= h >> 17; h ^= h << 5;
             const uint32_t deg = degf & kDegMask;
             if (deg == 0) break;
-            const Edge e = load_edge(adj, off + __umulhi(h, deg));  // one sector per jump
+            // one sector per jump, with the walkers' load policy (ld256_gather)
+#ifdef K6_PLAIN_LD
+            const Edge e = load_edge(adj, off + __umulhi(h, deg));
             cur = e.j; off = e.off; degf = e.deg_flags; dsum += e.d;
+#else
+            unsigned long long ea, eb, ec, ed;
+            ld256_gather(adj + (off + __umulhi(h, deg)), ea, eb, ec, ed);
+            cur = (uint32_t)ea; off = (uint32_t)(ea >> 32); degf = (uint32_t)eb;
+            dsum += __longlong_as_double((long long)ec);
+            (void)ed;
+#endif
         }
         acc += cur + (dsum == 0.5 ? 1 : 0);
     }

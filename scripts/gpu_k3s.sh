@@ -6,7 +6,7 @@
 TAG=$1; CFGS=$2; SHAPES=${3:-"auto 0 3"}
 OUT=gpurun_out/$TAG; mkdir -p $OUT
 export EXPMC_CSR_CACHE=/tmp/expmc_csr_cache
-for sh in 3 0; do
+for sh in ${TEST_SHAPES:-3 0 1}; do
   EXPMC_ENTRY_SHAPE=$sh timeout 900 python -m pytest tests/test_gpu_parity.py -x -q \
      -k "philox_walker_matches_cpu_model or gap_edge_cases or hub_rows or sharding or weighted" > $OUT/shape${sh}_tests.log 2>&1
   echo "shape $sh tests rc=$? $(tail -1 $OUT/shape${sh}_tests.log)" >> $OUT/summary.txt

@@ -129,6 +129,32 @@ def test_philox_walker_matches_cpu_model(pb, orc, graphs, W, splitting):
         assert np.array_equal(got.jumps, mj), name
 
 
+@pytest.mark.parametrize("shape", ["0", "1", "3"])
+def test_entry_kernel_shapes_share_the_contract(pb, orc, graphs, shape, monkeypatch):
+    """The launch shapes of the entry walker — entry_walk_kernel with 8 or 7
+    resident blocks (EXPMC_ENTRY_SHAPE 0 / 1) and the pipelined two-set
+    entry_pipe_kernel (3) — are schedules of one random-number and
+    accumulation contract: each must reproduce the CPU model bit for bit on
+    short walks, long walks (every walker jumps many times), weighted rows and
+    hub rows, whatever shape the launcher would have picked."""
+    monkeypatch.setenv("EXPMC_ENTRY_SHAPE", shape)
+    cases = [("fd2d_16", 1.0, 5000), ("fd2d_16", 3.0, 1000), ("ba_2000", 0.05, 10000),
+             ("weighted_40", 1.0, 4097), ("fd3d_10", 0.02, 1000), ("ws_3000", 0.05, 2000)]
+    for name, beta, W in cases:
+        csr = graphs[name]
+        m = pb.split(csr)
+        s = orc.split(csr)
+        v = pb.gen_vector(1, csr.n, 9)
+        rows = np.unique(np.linspace(0, csr.n - 1, min(csr.n, 40)).astype(np.uint32))
+        p = pb.PathParams(beta, 32, W, pb.Splitting.Strang, 11, pb.Rng.PHILOX)
+        got = pb.entries_estimate(m, v, rows, p)
+        mv, ms, mj = orc.fast_entries(s, v, rows, beta, 32, W, int(pb.Splitting.Strang), 11,
+                                      pb.entry_slots(W))
+        assert np.array_equal(got.values, mv), (shape, name, np.max(np.abs(got.values - mv)))
+        assert np.array_equal(got.std_errors, ms), (shape, name)
+        assert np.array_equal(got.jumps, mj), (shape, name)
+
+
 def _zcheck(z, K):
     z = np.asarray(z)
     bad = int(np.sum(np.abs(z) > 4.0))
