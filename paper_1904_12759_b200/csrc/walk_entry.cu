@@ -20,7 +20,9 @@
 //    are kept as deviations from a shift K (f0 when never-jumpers dominate),
 //    so they contribute exact zeros, and cost nothing: decisions cost ~1.6
 //    warp instructions per jumper instead of a quarter Philox per walker.
-//  * One dependent 32-B gather per jump through the fat adjacency (Edge).
+//  * One dependent 32-B gather per jump through the fat adjacency (Edge),
+//    marked L1::no_allocate (no L1 line per gather in flight: the shared-
+//    memory carveout no longer limits the gathers outstanding per SM).
 //  * Warp-cooperative scheduling over a stream of tasks.  Task t = (row
 //    t / WPR, part t % WPR).  A warp runs gap rounds (one Philox block per
 //    lane, 128 gaps) and appends the jumpers as tickets (first holding time,
@@ -33,6 +35,10 @@
 //    (exponent, exp() and deviation convergent over the batch, ticket k of
 //    the task on lane k mod 32, straight into that lane's running sums), and
 //    a task is finalized once its last batch is in.
+//  * One loop trip = jump (Philox, pick, gather issued) -> accumulate /
+//    finalize -> sojourn at the gathered state -> admit / pop.  The gather
+//    is consumed in the trip that issued it, after the accumulation work,
+//    and lands in registers nothing else writes (see the main loop).
 //  * Fixed accumulation order (result contract, replayed by
 //    oracle/fast_model.c): the jumpers of part w, numbered k = 0, 1, ... in
 //    increasing l, are summed by lane k mod 32 in increasing k; lanes are
@@ -66,29 +72,8 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef ENTRY_SWZ
 #define ENTRY_SWZ 0 // 1: swizzle the ticket ring (measured 1.5% slower: the conflicts are not the limiter)
 #endif
-#ifndef ENTRY_UNCOND_LD
-#define ENTRY_UNCOND_LD 1 // issue the jump gather for every lane (no predicated moves behind it)
-#endif
-#ifndef ENTRY_KEEP_J
-#define ENTRY_KEEP_J 1 // keep the unused word of the gathered slot live (no register moves behind the gather)
-#endif
-#ifndef ENTRY_ROTATE
-#define ENTRY_ROTATE 1 // loop trip = jump, accumulate/admit, then sojourn + pop (gather consumed in the trip that issued it)
-#endif
-#ifndef ENTRY_LATE_COPY
-#define ENTRY_LATE_COPY 1 // gather into fresh registers, copied into the state at the consumer
-#endif
 #ifndef ENTRY_TAB_SHARED
 #define ENTRY_TAB_SHARED 1 // exp table in shared memory (8-block shape)
-#endif
-#ifndef ENTRY_AHEAD
-#define ENTRY_AHEAD 0 // (measured slower: cfg5 +4.8%, cfg4 +2.6%) claim tasks one ahead: row index loaded and record prefetched a task early
-#endif
-#ifndef ENTRY_EARLY_ADMIT
-#define ENTRY_EARLY_ADMIT 0 // (measured slower: cfg5 +5%, cfg2 +20%) rotated loop: admit before the sojourn while fewer tickets are queued (0: off)
-#endif
-#ifndef ENTRY_LOOKAHEAD
-#define ENTRY_LOOKAHEAD 0 // (measured: cfg4 +1%, cfg1 +27%) 7-block (long-walk) shape: Philox block of the next jump drawn a trip ahead
 #endif
 #ifndef ENTRY_POP_MIN
 #define ENTRY_POP_MIN 2 // run the scheduler once this many lanes are idle
@@ -203,17 +188,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     // the current state as the raw 32-byte Edge slot it was gathered from
     // ({j, off}, {deg_flags, inv_rate}, d, v)
     unsigned long long ea = 0, eb = 0, ec = 0, ed = 0;
-#if ENTRY_LATE_COPY
-    // the slot being gathered: fresh registers written only by the load, and
-    // copied into the state by pinned (volatile) moves at the consumer, so
-    // that no register move of loaded data sits behind the load itself
+    // the slot being gathered: registers written only by the load, copied
+    // into the state by pinned (volatile) moves at the consumer
     unsigned long long la = 0, lb = 0, lc = 0, ld = 0;
-#endif
-    // lookahead (long-walk shape): the next jump's Philox block, whether the
-    // lane has one, and whether it jumped in this trip
-    constexpr bool kLookahead = ENTRY_LOOKAHEAD && ENTRY_ROTATE && ENTRY_LATE_COPY && BL <= 7;
-    uint32_t nbx = 0, nby = 0, nbz = 0, nbw = 0;
-    bool ready = false, go = false;
 #define OFF ((uint32_t)(ea >> 32))
 #define DEGF ((uint32_t)eb)
 #define IR (__uint_as_float((uint32_t)(eb >> 32)))
@@ -236,16 +213,11 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, DCUR)) : S;
             q.v[pos] = VCUR;
             q.tk[tk_slot(pos)].x = jc;
-#if ENTRY_KEEP_J
-            // The landing row id (word 0 of the gathered slot) is not needed,
-            // and ptxas compacts the registers of a load with a dead word by
-            // moves placed right behind the load: the warp then waits for the
-            // gather before the accumulation / admission work instead of
-            // after it (24.7% of the stall samples sat on that move,
-            // profiles/r02).  A store of the word to the sink slot on this
-            // path keeps all eight registers in place.
+            // (the landing row id, word 0 of the gathered slot, is not needed
+            // by the walk: storing it to the sink slot keeps the word live,
+            // so its register is not reused — and waited on — right behind
+            // the load)
             q.tk[CAP].y = (uint32_t)ea;
-#endif
             act = false;
             fin = true;
         } else {
@@ -269,45 +241,18 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         return anext + tstride;
 #endif
     };
-#if ENTRY_AHEAD
-    // Tasks are claimed one ahead: `anext` with its row index `inext` loaded
-    // when the previous task was claimed (the load lands during a whole
-    // task), and the row's record and rate prefetched into L2 when it becomes
-    // `atask` — open_task then finds them instead of waiting for two
-    // dependent DRAM round trips (rows[] -> rec[], rate[]).
-    auto load_row = [&](uint32_t t) -> uint32_t { return t < ntask ? __ldg(rows + t / WPR) : 0u; };
-    uint32_t irow = load_row(atask);
-    uint32_t anext = atask;
-    anext = next_task();
-    uint32_t inext = load_row(anext);
-    auto advance_task = [&] {
-        atask = anext;
-        irow = inext;
-        if (atask < ntask) {
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(rec + irow));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(rate + irow));
-        }
-        anext = next_task();
-        inext = load_row(anext);
-    };
-#else
     uint32_t anext = atask;
     auto advance_task = [&] {
         anext = atask;
         atask = next_task();
     };
-#endif
 
     // Open task `atask` in slot tw: row constants computed by two lanes in
     // parallel (lane 0: e^{-λ}, lane 1: e^{β d}).  Part w of a row owns the
     // walkers [⌊wW/WPR⌋, ⌊(w+1)W/WPR⌋).
     auto open_task = [&] {
         const int sl = (int)(tw & (RT - 1));
-#if ENTRY_AHEAD
-        const uint32_t i = irow;
-#else
         const uint32_t i = rows[atask / WPR];
-#endif
         const RowRec ri = load_rec(rec, i);
         const double lam = __dmul_rn(__ldg(rate + i), p.beta);
         const double ex = exp_det(lane == 0 ? -lam : __dmul_rn(p.beta, ri.d));
@@ -421,60 +366,25 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     };
 
     while (true) {
-#if ENTRY_ROTATE
-#define JMP act
-        // ---- C: one jump for every walker whose sojourn did not end the path.
-        // After the pop every walker still in flight must jump (jmp == act),
-        // so the gather is issued unconditionally (idle lanes re-read slot 0
-        // and are re-initialised at their next pop): the 256-bit load then
-        // lands straight in the loop-carried registers, with no predicated
-        // register moves right behind it to stall on, and its latency hides
-        // behind the accumulation / admission work below until the next
-        // iteration's sojourn reads the new state.
-#if ENTRY_UNCOND_LD
+        // ---- one jump for every walker in flight.  The trip runs jump ->
+        // accumulate / finalize -> sojourn -> admit / pop, so the gather issued
+        // here is consumed in the same trip, after the accumulation work: it
+        // lands in registers (la..ld) that nothing else writes, copied into
+        // the walker's state by pinned moves just before the sojourn.  (With
+        // the gather landing in the loop-carried state itself, ptxas compacted
+        // the slot's dead word away by register moves right behind the load,
+        // and every warp waited for its gather *before* the accumulation work:
+        // 24.7% of the stall samples, profiles/r02.)  Idle lanes re-read slot
+        // 0: no predicated moves behind the load either.
         {
-#else
-        if (JMP) {
-#endif
-#if ENTRY_LOOKAHEAD
-            // Long-walk shape: the Philox block of a jump is drawn one trip
-            // ahead, off the gather -> sojourn -> jump chain (it depends on
-            // the jump count, not on the gathered state), and computed while
-            // this trip's gather is in flight.  A popped walker waits one
-            // trip for its first block (1 trip in ~β·rate).
-            if (kLookahead) {
-                go = act && ready;
-                const uint32_t off = OFF, degf = DEGF;
-                uint32_t k = pick_index(nby, nbw, degf & kDegMask);
-                if (go && (degf & kNonUniform) && nbz >= __ldg(thr + off + k))
-                    k = __ldg(alias + off + k);
-                ld256_gather(adj + (go ? off + k : 0u), la, lb, lc, ld);
-                if (go) {
-                    ew = nbx;
-                    ++jc;
-                }
-                const U4 B = philox4x32_10(U4{jc, wl, wi, kTagEntry}, p.rk);
-                nbx = B.x;
-                nby = B.y;
-                nbz = B.z;
-                nbw = B.w;
-                ready = act;
-            } else
-#endif
-            {
             const U4 B = philox4x32_10(U4{jc, wl, wi, kTagEntry}, p.rk);
             const uint32_t off = OFF, degf = DEGF;
             uint32_t k = pick_index(B.y, B.w, degf & kDegMask);
-            if (JMP && (degf & kNonUniform) && B.z >= __ldg(thr + off + k))
+            if (act && (degf & kNonUniform) && B.z >= __ldg(thr + off + k))
                 k = __ldg(alias + off + k);
-#if ENTRY_LATE_COPY
-            ld256_gather(adj + (JMP ? off + k : 0u), la, lb, lc, ld);
-#else
-            ld256(adj + (JMP ? off + k : 0u), ea, eb, ec, ed);
-#endif
+            ld256_gather(adj + (act ? off + k : 0u), la, lb, lc, ld);
             ew = B.x;
             ++jc;
-            }
         }
         // ---- accumulate finished tickets in batches of 32 (lane = ticket -
         // tstart mod 32) and finalize completed tasks, oldest first.  Tickets
@@ -545,91 +455,14 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         }
         }
         if (tf == tw && !aopen && atask >= ntask) break;  // every task finalized
-#if ENTRY_EARLY_ADMIT
-        // gap rounds ahead of need (fewer than a warp's worth of tickets
-        // queued), while this trip's gather is still in flight
-        while (can_admit() && tail - head < (uint32_t)ENTRY_EARLY_ADMIT) admit();
-#endif
-        // ---- A: sojourn of every walker in flight
+        // ---- sojourn of every walker in flight, at the state just gathered
         bool fin = false, jmp = false;
-#if ENTRY_LATE_COPY
-        if (kLookahead ? go : act) {
-            asm volatile("mov.b64 %0, %4;\n\tmov.b64 %1, %5;\n\tmov.b64 %2, %6;\n\tmov.b64 %3, %7;"
-                         : "=l"(ea), "=l"(eb), "=l"(ec), "=l"(ed)
-                         : "l"(la), "l"(lb), "l"(lc), "l"(ld));
-            sojourn(neg_ln_u(ew), fin, jmp);
-        }
-#else
-        if (act) sojourn(neg_ln_u(ew), fin, jmp);
-#endif
-        unsigned idle = __ballot_sync(FULL, !act);
-        // scheduler work only when enough lanes are free (batching pops
-        // amortises the scheduler over several walkers)
-        if (__popc(idle) < ENTRY_POP_MIN && idle != FULL) idle = 0;
-        if (idle) {
-            // ---- admit: sweep chunks while queued tickets cannot feed the
-            // idle lanes and a whole chunk's tickets fit in the ring
-            while (can_admit() && tail - head < (uint32_t)__popc(idle)) admit();
-            // ---- pop: idle lanes take tickets in order
-            const uint32_t avail = tail - head;
-            const uint32_t nidle = (uint32_t)__popc(idle);
-            const uint32_t take = avail < nidle ? avail : nidle;
-            const uint32_t rank = (uint32_t)__popc(idle & lt);
-            if (!act && rank < take) {
-                tk = head + rank;
-                const uint2 t2 = q.tk[tk_slot(tk & (CAP - 1))];
-                wl = t2.y & 0x1fffffffu;
-                const TaskRec& m = q.task[t2.y >> 29];
-                const uint4 r0 = *reinterpret_cast<const uint4*>(&m.rr);  // off, degf, ir, -
-                ea = (unsigned long long)r0.x << 32;
-                eb = r0.y | ((unsigned long long)r0.z << 32);
-                ec = (unsigned long long)__double_as_longlong(m.rr.d);
-                ed = (unsigned long long)__double_as_longlong(m.rr.v);
-                wi = m.i;
-                t = 0.0; S = 0.0; G = 0.0; jc = 0;
-                act = true;
-                ready = false;
-                // a jumper's first sojourn (R < λ) ends in a jump, so it joins
-                // this iteration's jump
-                sojourn(__uint_as_float(t2.x), fin, jmp);
-            }
-            head += take;
-#ifdef ENTRY_STATS
-            if (lane == 0) {
-                atomicAdd(p.stats + 1, (unsigned long long)nidle);
-                if (avail < nidle) {  // lanes left idle: why?
-                    atomicAdd(p.stats + 2, (unsigned long long)(nidle - avail));
-                    if (atask < ntask) atomicAdd(p.stats + 3, 1ull);  // ring full
-                }
-            }
-#endif
-        }
-#ifdef ENTRY_STATS
-        {
-            const unsigned jb = __ballot_sync(FULL, jmp);
-            const unsigned ab = __ballot_sync(FULL, act);
-            if (lane == 0) {
-                atomicAdd(p.stats + 0, 1ull);
-                atomicAdd(p.stats + 4, (unsigned long long)__popc(jb));
-                atomicAdd(p.stats + 5, (unsigned long long)__popc(ab));
-            }
-        }
-#endif
-#undef JMP
-#else
-#define JMP jmp
-        // ---- A: sojourn of every walker in flight
-        bool fin = false, jmp = false;
-#if ENTRY_LATE_COPY
         if (act) {
             asm volatile("mov.b64 %0, %4;\n\tmov.b64 %1, %5;\n\tmov.b64 %2, %6;\n\tmov.b64 %3, %7;"
                          : "=l"(ea), "=l"(eb), "=l"(ec), "=l"(ed)
                          : "l"(la), "l"(lb), "l"(lc), "l"(ld));
             sojourn(neg_ln_u(ew), fin, jmp);
         }
-#else
-        if (act) sojourn(neg_ln_u(ew), fin, jmp);
-#endif
         unsigned idle = __ballot_sync(FULL, !act);
         // scheduler work only when enough lanes are free (batching pops
         // amortises the scheduler over several walkers)
@@ -657,7 +490,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 t = 0.0; S = 0.0; G = 0.0; jc = 0;
                 act = true;
                 // a jumper's first sojourn (R < λ) ends in a jump, so it joins
-                // this iteration's jump
+                // the next trip's jump
                 sojourn(__uint_as_float(t2.x), fin, jmp);
             }
             head += take;
@@ -681,103 +514,6 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 atomicAdd(p.stats + 5, (unsigned long long)__popc(ab));
             }
         }
-#endif
-        // ---- C: one jump for every walker whose sojourn did not end the path.
-        // After the pop every walker still in flight must jump (jmp == act),
-        // so the gather is issued unconditionally (idle lanes re-read slot 0
-        // and are re-initialised at their next pop): the 256-bit load then
-        // lands straight in the loop-carried registers, with no predicated
-        // register moves right behind it to stall on, and its latency hides
-        // behind the accumulation / admission work below until the next
-        // iteration's sojourn reads the new state.
-#if ENTRY_UNCOND_LD
-        {
-#else
-        if (JMP) {
-#endif
-            const U4 B = philox4x32_10(U4{jc, wl, wi, kTagEntry}, p.rk);
-            const uint32_t off = OFF, degf = DEGF;
-            uint32_t k = pick_index(B.y, B.w, degf & kDegMask);
-            if (JMP && (degf & kNonUniform) && B.z >= __ldg(thr + off + k))
-                k = __ldg(alias + off + k);
-#if ENTRY_LATE_COPY
-            ld256_gather(adj + (JMP ? off + k : 0u), la, lb, lc, ld);
-#else
-            ld256(adj + (JMP ? off + k : 0u), ea, eb, ec, ed);
-#endif
-            ew = B.x;
-            ++jc;
-        }
-        // ---- accumulate finished tickets in batches of 32 (lane = ticket -
-        // tstart mod 32) and finalize completed tasks, oldest first.  Tickets
-        // [xc, xc + rdy) are popped and finished: the oldest ticket still
-        // walking (or the first not popped) bounds them.
-        const uint32_t minoff = __reduce_min_sync(FULL, act ? tk - xc : ~0u);
-        uint32_t rdy = head - xc < minoff ? head - xc : minoff;
-        if (rdy >= 32u || (ocl && rdy >= oend - xc)) {
-        __syncwarp();
-        while (tf != tw) {
-            const TaskRec& m = q.task[tf & (RT - 1)];
-            // ready tickets of this task (offsets from xc)
-            const uint32_t lim = ocl && oend - xc < rdy ? oend - xc : rdy;
-            uint32_t nb;
-            if (lim >= 32u) {
-                nb = 32u;                     // a full batch
-            } else if (ocl && lim == oend - xc) {
-                nb = lim;                     // the closed task's last (partial) batch
-            } else {
-                break;                        // wait for more tickets
-            }
-            if (nb) {
-                if ((uint32_t)lane < nb) {
-                    const uint32_t pos = (xc + lane) & (CAP - 1);
-                    const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], m.corr));
-                    const double dv = __dsub_rn(
-                        __dmul_rn(kTabShared ? exp_det_tab(x, s_tab, false) : exp_det(x), q.v[pos]),
-                        m.K);
-                    s1 = __dadd_rn(s1, dv);
-                    s2 = __fma_rn(dv, dv, s2);
-                    jsum += q.tk[tk_slot(pos)].x;
-                }
-                xc += nb;
-                rdy -= nb;
-            }
-            if (!ocl || xc != oend) continue;
-            // task complete: butterfly, never-jumpers, output
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                s1 = __dadd_rn(s1, __shfl_xor_sync(FULL, s1, o));
-                s2 = __dadd_rn(s2, __shfl_xor_sync(FULL, s2, o));
-                jsum += __shfl_xor_sync(FULL, jsum, o);
-            }
-            if (lane == 0) {
-                // never-jumpers score f0: deviation f0 - K each (0 when K = f0)
-                const double f0 = m.f0, K = m.K;
-                const uint32_t n0 = m.n0;
-                const double c = __dsub_rn(f0, K);
-                if (n0 != 0 && c != 0.0) {
-                    s1 = __fma_rn((double)n0, c, s1);
-                    s2 = __fma_rn((double)n0, __dmul_rn(c, c), s2);
-                }
-                // the divisions and sqrt of the estimate run in the
-                // row-parallel combine pass, not on one lane here
-                partial[m.task] = make_double4(s1, s2, __longlong_as_double((long long)jsum), K);
-            }
-            s1 = 0.0;
-            s2 = 0.0;
-            jsum = 0;
-            ++tf;
-            __syncwarp();
-            ocl = false;
-            if (tf != tw) {
-                const uint2 e = *reinterpret_cast<const uint2*>(&q.task[tf & (RT - 1)].tend);
-                ocl = e.y != 0u;
-                oend = e.x;
-            }
-        }
-        }
-        if (tf == tw && !aopen && atask >= ntask) break;  // every task finalized
-#undef JMP
 #endif
     }
 }
