@@ -79,6 +79,25 @@ constexpr unsigned FULL = 0xffffffffu;
 #define ENTRY_POP_MIN 2 // run the scheduler once this many lanes are idle
 #endif
 
+// Self-checking build (make variants VARIANTS="checks:-DEXPMC_CHECKS"): the
+// invariants of the warp-synchronous ticket ring, asserted on the device.
+// compute-sanitizer is closed on this pool (profiles/r02/sanitizer_closed_*),
+// so this build, run under the bit-exact model tests with every launch shape
+// and row sharding, is the race / bounds evidence (scripts/gpu_checks.sh).
+#ifdef EXPMC_CHECKS
+#define CHK(c)                                                                          \
+    do {                                                                                \
+        if (!(c)) {                                                                     \
+            printf("K3 check failed: %s (line %d) block %d thread %d\n", #c, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                  \
+            __trap();                                                                   \
+        }                                                                               \
+    } while (0)
+constexpr unsigned long long kUnfinished = 0x7ff8dead00000001ull;  // NaN: ticket popped, not parked
+#else
+#define CHK(c) ((void)0)
+#endif
+
 // Physical slot of ticket position `pos` in the tk ring.  A gap round
 // stores ticket (lane, k) at tail + 4 lane + k: 8-byte slots 32 bytes apart
 // hit 4 bank pairs (8-way conflicts).  XOR-ing bits 4-5 into bits 0-1
@@ -210,6 +229,10 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             // park the raw weight sum; the exponent is formed at accumulation
             S = __fma_rn(DCUR, __dsub_rn(p.n_grid1, G), S);
             const uint32_t pos = tk & (CAP - 1);
+            CHK(tk - xc < CAP && tail - tk - 1u < CAP);  // in the ring, not yet accumulated
+#ifdef EXPMC_CHECKS
+            CHK((unsigned long long)__double_as_longlong(q.S[pos]) == kUnfinished);  // parked once
+#endif
             q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, DCUR)) : S;
             q.v[pos] = VCUR;
             q.tk[tk_slot(pos)].x = jc;
@@ -310,6 +333,8 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         }
         const uint32_t sl = (tw - 1) & (RT - 1);
         const TaskRec& a = q.task[sl];
+        CHK(tail + kRound - xc <= CAP && tw - tf >= 1u && tw - tf <= (uint32_t)RT);
+        CHK(a.task == atask && a.closed == 0u);
         const float lamf = a.lam, ilam = __uint_as_float(a.rr.spare);
         const U4 D = philox4x32_10(
             U4{0xfffffff0u | (atask % WPR), 32u * around + (uint32_t)lane, a.i, kTagEntry}, p.rk);
@@ -344,8 +369,22 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             const bool ok = P < anw;
             cnt += __popc(__ballot_sync(FULL, ok));
             const uint32_t pos = ok ? ((tail + 4u * lane + k) & (CAP - 1)) : CAP;
+            // valid tickets form a prefix in (lane, k) order and stay inside the part
+            CHK(!ok || (tail + 4u * lane + k - xc < CAP && al0 + P < (1u << 29)));
             q.tk[tk_slot(pos)] = make_uint2(__float_as_uint(R[k]), (sl << 29) | (al0 + P));
         }
+#ifdef EXPMC_CHECKS
+        {   // the valid tickets of the round are exactly positions [tail, tail + cnt)
+            uint32_t mine = 0;
+            for (int k = 0; k < 4; ++k) mine += (apos + exc + off[k] < anw) ? 1u : 0u;
+            const uint32_t before = __reduce_add_sync(FULL, mine) - 0u;
+            CHK(before == cnt);
+            const bool prefix_ok = mine == 4u || (apos + exc + off[mine] >= anw);
+            CHK(prefix_ok);
+            const uint32_t full_before = __popc(__ballot_sync(FULL, mine == 4u) & lt);
+            CHK(mine == 0u || full_before == (uint32_t)lane);  // every earlier lane is full
+        }
+#endif
         tail += cnt;
         apos = min(apos + total, 0x7fffffffu);
         ++around;
@@ -382,6 +421,10 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             uint32_t k = pick_index(B.y, B.w, degf & kDegMask);
             if (act && (degf & kNonUniform) && B.z >= __ldg(thr + off + k))
                 k = __ldg(alias + off + k);
+#ifdef EXPMC_CHECKS
+            CHK(!act || ((degf & kDegMask) != 0u && k < (degf & kDegMask) &&
+                         (uint64_t)off + k < (uint64_t)(uintptr_t)p.stats));  // p.stats: nnz
+#endif
             ld256_gather(adj + (act ? off + k : 0u), la, lb, lc, ld);
             ew = B.x;
             ++jc;
@@ -407,8 +450,14 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 break;                        // wait for more tickets
             }
             if (nb) {
+                CHK(xc + nb - xc <= head - xc && nb <= 32u);
                 if ((uint32_t)lane < nb) {
                     const uint32_t pos = (xc + lane) & (CAP - 1);
+#ifdef EXPMC_CHECKS
+                    // every ticket of the batch was popped and parked
+                    CHK((unsigned long long)__double_as_longlong(q.S[pos]) != kUnfinished);
+                    CHK((q.tk[tk_slot(pos)].y >> 29) == (tf & (RT - 1)));  // ...and is this task's
+#endif
                     const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], m.corr));
                     const double dv = __dsub_rn(
                         __dmul_rn(kTabShared ? exp_det_tab(x, s_tab, false) : exp_det(x), q.v[pos]),
@@ -439,6 +488,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 }
                 // the divisions and sqrt of the estimate run in the
                 // row-parallel combine pass, not on one lane here
+                CHK(m.task < ntask && m.closed == 1u && m.tend == xc);
                 partial[m.task] = make_double4(s1, s2, __longlong_as_double((long long)jsum), K);
             }
             s1 = 0.0;
@@ -481,6 +531,11 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 const uint2 t2 = q.tk[tk_slot(tk & (CAP - 1))];
                 wl = t2.y & 0x1fffffffu;
                 const TaskRec& m = q.task[t2.y >> 29];
+                CHK(tk - xc < CAP && tail - tk - 1u < CAP);             // ticket is in the ring
+                CHK((((t2.y >> 29) - tf) & (RT - 1)) < tw - tf);        // its task is in flight
+#ifdef EXPMC_CHECKS
+                q.S[tk & (CAP - 1)] = __longlong_as_double((long long)kUnfinished);
+#endif
                 const uint4 r0 = *reinterpret_cast<const uint4*>(&m.rr);  // off, degf, ir, -
                 ea = (unsigned long long)r0.x << 32;
                 eb = r0.y | ((unsigned long long)r0.z << 32);
@@ -631,8 +686,15 @@ int launch_t(const char* name, const DevSplit& m, const uint32_t* rows, uint64_t
 #if ENTRY_DYNAMIC
     cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s);
 #endif
+#ifdef EXPMC_CHECKS
+    FastParams pc = p;  // checks build: the gather bound (nnz) travels in the unused stats slot
+    pc.stats = reinterpret_cast<unsigned long long*>((uintptr_t)m.nnz);
+    KERN<<<grid, 128, pad, s>>>(m.rec, m.rate, m.adj, m.alias_thr, m.alias_idx, rows, nrows, pc,
+                                partial, ctr);
+#else
     KERN<<<grid, 128, pad, s>>>(m.rec, m.rate, m.adj, m.alias_thr, m.alias_idx, rows, nrows, p,
                                 partial, ctr);
+#endif
     combine_parts_kernel<WPR><<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(
         partial, nrows, p.W, value, se, jumps);
     return 2;
