@@ -284,7 +284,10 @@ def test_bench_reference_arm_cpu(ref, pb, cfg, scale):
     for k in ("metric", "unit", "cpu_baseline", "e2e", "config", "higher_is_better"):
         assert k in line
     cb = line["cpu_baseline"]
-    assert cb["kind"] == "reference" and cb["path_only_value"] >= line["value"] * 0.999
+    # path-only rate: a few rows at samples = F W minus the same rows at
+    # samples = 1 (None when the walkers stay below the timing noise)
+    assert cb["kind"] == "reference" and "path_only_how" in cb
+    assert cb["path_only_value"] is None or cb["path_only_value"] > 0
     assert 0.0 <= cb["setup_share"] <= 1.0 and cb["setup_per_call_s"] > 0
     sys.path.insert(0, ROOT)
     import bench
