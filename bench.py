@@ -371,6 +371,7 @@ def main():
         return pb.PathParams(cfg.beta, cfg.n_steps, cfg.walkers, pb.Splitting.Strang,
                              args.seed + step, pb.Rng.PHILOX)
 
+    contiguous = cfg.rows is None and nrows > 0  # a rank's block of all rows
     K, Wm = args.steps, args.warmup
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(K)]
@@ -378,8 +379,12 @@ def main():
     def step(k, timed):
         if timed:
             evs[k][0].record(stream)
-        pb.entries_device(m, rows_d.data_ptr(), nrows, params(k), val.data_ptr(),
-                          se.data_ptr(), jm.data_ptr(), sp)
+        if contiguous:  # all rows / a rank's block of them: no row array on the device
+            pb.entries_device_range(m, int(rows[0]), nrows, params(k), val.data_ptr(),
+                                    se.data_ptr(), jm.data_ptr(), sp)
+        else:
+            pb.entries_device(m, rows_d.data_ptr(), nrows, params(k), val.data_ptr(),
+                              se.data_ptr(), jm.data_ptr(), sp)
         if timed:
             evs[k][1].record(stream)
         jtot.add_(jm.sum())  # warm-up runs it too (lazy module load)

@@ -181,6 +181,12 @@ int expmc_cuda_set_v_device(expmc_matrix* m, const double* v_dev, uint64_t nv, v
 int expmc_cuda_entries_device(expmc_matrix* m, const uint32_t* rows_dev, uint64_t nrows,
                               const expmc_path_params* p, double* value_dev,
                               double* std_error_dev, uint64_t* jumps_dev, void* stream);
+/* Same over the contiguous rows [row_lo, row_lo + nrows) (range-checked): no
+ * row array — the walker derives a task's row from its index.  Bitwise the
+ * same results as the listed form. */
+int expmc_cuda_entries_device_range(expmc_matrix* m, uint64_t row_lo, uint64_t nrows,
+                                    const expmc_path_params* p, double* value_dev,
+                                    double* std_error_dev, uint64_t* jumps_dev, void* stream);
 /* K6 gather ceiling: chains_per_row chains of chain_len jumps from every
  * listed row (memory-only walker, same access pattern as K3), async. */
 int expmc_cuda_gather_ceiling_device(expmc_matrix* m, const uint32_t* rows_dev, uint64_t nrows,

@@ -8,7 +8,7 @@ The reference's estimator API (arXiv 1904.12759 C++ artifact,
 from ._lib import ExpmcError, lib
 from .estimator import (EntriesEstimate, binomial_samples, last_jumpers, last_k4_stats, start_counts, tc_estimate_rows,
                         vector_estimate_rows, finalize, Estimate, PathParams, Rng, SplitMatrix, Splitting,
-                        VectorEstimate, entries_device, entries_estimate, entries_estimate_multi, entry_estimate,
+                        VectorEstimate, entries_device, entries_device_range, entries_estimate, entries_estimate_multi, entry_estimate,
                         invalidate_v, set_v_cache, v_stagings, exp_law,
                         entry_slots, expmv, from_entries, from_matrix_market, gather_ceiling_device, launch_count, set_v_device,
                         split, splitting_product, tc_estimate, vector_estimate)
@@ -20,7 +20,7 @@ from .spectral import BetaRule, lambda_max, resolve_beta
 __all__ = [
     "ExpmcError", "lib", "binomial_samples", "last_jumpers", "last_k4_stats", "start_counts", "tc_estimate_rows",
     "vector_estimate_rows", "finalize", "EntriesEstimate", "Estimate", "PathParams", "Rng", "SplitMatrix",
-    "Splitting", "VectorEstimate", "entries_device", "entries_estimate", "entries_estimate_multi",
+    "Splitting", "VectorEstimate", "entries_device", "entries_device_range", "entries_estimate", "entries_estimate_multi",
     "entry_estimate", "invalidate_v", "set_v_cache", "v_stagings", "exp_law",
     "entry_slots", "expmv", "gather_ceiling_device", "launch_count", "set_v_device", "split",
     "splitting_product", "tc_estimate", "vector_estimate", "Csr", "build_config",

@@ -73,6 +73,8 @@ SIGNATURES = [
     ("expmc_cuda_set_v_device", C.c_int, [vp, vp, C.c_uint64, vp]),
     ("expmc_cuda_entries_device", C.c_int,
      [vp, vp, C.c_uint64, C.POINTER(PathParamsC), vp, vp, vp, vp]),
+    ("expmc_cuda_entries_device_range", C.c_int,
+     [vp, C.c_uint64, C.c_uint64, C.POINTER(PathParamsC), vp, vp, vp, vp]),
     ("expmc_cuda_gather_ceiling_device", C.c_int,
      [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, vp]),
     ("expmc_cuda_entry_slots", C.c_uint32, [C.c_uint64]),

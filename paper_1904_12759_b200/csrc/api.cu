@@ -674,11 +674,13 @@ void run_entries(expmc_matrix* h, const double* v, uint64_t nv, const uint32_t* 
         void* scratch =
             h->part.get<unsigned char>(entry_fast_scratch_bytes((nrows + pieces - 1) / pieces,
                                                                 p->samples));
-        const FastParams fp = fast_params(p, p->samples);
+        FastParams fp = fast_params(p, p->samples);
         for (uint64_t k = 0; k < pieces; ++k) {
             const uint64_t lo = nrows * k / pieces, hi = nrows * (k + 1) / pieces;
-            int kl = launch_entry_fast(h->m, rd + lo, hi - lo, fp, ov + lo, os + lo, oj + lo,
-                                             scratch, s);
+            // all rows (rows == NULL): the contiguous-range form, no row array
+            fp.row0 = (uint32_t)lo;
+            int kl = launch_entry_fast(h->m, rows ? rd + lo : nullptr, hi - lo, fp, ov + lo,
+                                       os + lo, oj + lo, scratch, s);
             if (total_jumps) {
                 launch_sum_u64(hi - lo, oj + lo, jtot, s);
                 ++kl;
@@ -1405,6 +1407,32 @@ int expmc_cuda_entries_device(expmc_matrix* h, const uint32_t* rows_dev, uint64_
         const int k = launch_entry_fast(h->m, rows_dev, nrows, fast_params(p, p->samples),
                                         value_dev, std_error_dev, jumps_dev, scratch,
                                         pick_stream(h, stream));
+        after_launch(k);
+    });
+}
+
+int expmc_cuda_entries_device_range(expmc_matrix* h, uint64_t row_lo, uint64_t nrows,
+                                    const expmc_path_params* p, double* value_dev,
+                                    double* std_error_dev, uint64_t* jumps_dev, void* stream) {
+    return guarded([&] {
+        if (!h) throw InvalidArg("matrix handle is null");
+        std::lock_guard<std::mutex> lk(h->mu);
+        validate_params(p);
+        if (p->rng != EXPMC_RNG_PHILOX)
+            throw InvalidArg("entries_device supports the Philox walker only");
+        if (row_lo > h->m.n || nrows > h->m.n - row_lo) throw InvalidArg("entry index out of range");
+        DeviceGuard g(h->device);
+        if (p->samples >= (1ull << 29)) {  // large-W grouped path: needs the row list
+            run_entries_big(h, all_rows(h) + row_lo, nrows, p, value_dev, std_error_dev,
+                            jumps_dev, pick_stream(h, stream));
+            return;
+        }
+        if (nrows >= (1ull << 30)) throw InvalidArg("at most 2^30 rows per call");
+        void* scratch = h->part.get<unsigned char>(entry_fast_scratch_bytes(nrows, p->samples));
+        FastParams fp = fast_params(p, p->samples);
+        fp.row0 = (uint32_t)row_lo;
+        const int k = launch_entry_fast(h->m, nullptr, nrows, fp, value_dev, std_error_dev,
+                                        jumps_dev, scratch, pick_stream(h, stream));
         after_launch(k);
     });
 }

@@ -48,6 +48,7 @@ struct FastParams {
     // rounds read them as constant-bank operands instead of registers.
     PhiloxKeys rk;
     unsigned long long* stats = nullptr;  // ENTRY_STATS builds only
+    uint32_t row0 = 0;  // K3 with rows == nullptr: the launch covers rows [row0, row0 + nrows)
 };
 
 // split_pack.cu

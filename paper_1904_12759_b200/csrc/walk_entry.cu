@@ -275,7 +275,8 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     // walkers [⌊wW/WPR⌋, ⌊(w+1)W/WPR⌋).
     auto open_task = [&] {
         const int sl = (int)(tw & (RT - 1));
-        const uint32_t i = rows[atask / WPR];
+        // listed rows, or (rows == nullptr) the contiguous range from p.row0
+        const uint32_t i = rows ? rows[atask / WPR] : p.row0 + atask / WPR;
         const RowRec ri = load_rec(rec, i);
         const double lam = __dmul_rn(__ldg(rate + i), p.beta);
         const double ex = exp_det(lane == 0 ? -lam : __dmul_rn(p.beta, ri.d));

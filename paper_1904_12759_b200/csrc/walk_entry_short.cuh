@@ -130,7 +130,7 @@ entry_pipe_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
 
     auto open_task = [&] {
         const int sl = (int)(tw & (RT - 1));
-        const uint32_t i = rows[atask / WPR];
+        const uint32_t i = rows ? rows[atask / WPR] : p.row0 + atask / WPR;
         const RowRec ri = load_rec(rec, i);
         const double lam = __dmul_rn(__ldg(rate + i), p.beta);
         const double ex = exp_det(lane == 0 ? -lam : __dmul_rn(p.beta, ri.d));

@@ -417,6 +417,15 @@ def entries_device(m: SplitMatrix, rows_ptr: int, nrows: int, p: PathParams, val
                                           se_ptr, jumps_ptr, stream or None))
 
 
+def entries_device_range(m: SplitMatrix, row_lo: int, nrows: int, p: PathParams, value_ptr: int,
+                         se_ptr: int, jumps_ptr: int, stream: int = 0) -> None:
+    """entries_device over the contiguous rows [row_lo, row_lo + nrows): no row
+    array on the device; same results bit for bit."""
+    pc = p._c()
+    check(lib().expmc_cuda_entries_device_range(m.handle, int(row_lo), int(nrows), C.byref(pc),
+                                                value_ptr, se_ptr, jumps_ptr, stream or None))
+
+
 def gather_ceiling_device(m: SplitMatrix, rows_ptr: int, nrows: int, chains_per_row: int,
                           chain_len: int, stream: int = 0) -> None:
     check(lib().expmc_cuda_gather_ceiling_device(m.handle, rows_ptr, nrows,

@@ -365,6 +365,44 @@ def test_device_api_matches_host_api(pb, graphs):
     assert np.array_equal(jm.cpu().numpy().astype(np.uint64), host.jumps)
 
 
+def test_contiguous_range_entry_matches_listed_rows(pb, graphs):
+    """expmc_cuda_entries_device_range (rows [lo, lo + n), no row array) gives
+    the bits of the listed form, on an interior range too."""
+    import torch
+
+    csr = graphs["ba_2000"]
+    m = pb.split(csr)
+    v = pb.gen_vector(1, csr.n, 9)
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    v_d = torch.from_numpy(v).to(dev)
+    pb.set_v_device(m, v_d.data_ptr(), csr.n, st)
+    p = pb.PathParams(0.05, 32, 3000, pb.Splitting.Strang, 21, pb.Rng.PHILOX)
+    for lo, n in ((0, csr.n), (137, 901), (csr.n - 5, 5)):
+        rows = torch.arange(lo, lo + n, dtype=torch.int32, device=dev)
+        out = []
+        for form in ("listed", "range"):
+            val = torch.empty(n, dtype=torch.float64, device=dev)
+            se = torch.empty_like(val)
+            jm = torch.empty(n, dtype=torch.int64, device=dev)
+            if form == "listed":
+                pb.entries_device(m, rows.data_ptr(), n, p, val.data_ptr(), se.data_ptr(),
+                                  jm.data_ptr(), st)
+            else:
+                pb.entries_device_range(m, lo, n, p, val.data_ptr(), se.data_ptr(),
+                                        jm.data_ptr(), st)
+            torch.cuda.synchronize()
+            out.append((val.cpu().numpy(), se.cpu().numpy(), jm.cpu().numpy()))
+        for a, b in zip(*out):
+            assert np.array_equal(a, b), (lo, n)
+    with pytest.raises(ValueError, match="entry index out of range"):
+        pb.entries_device_range(m, csr.n - 2, 3, p, 0, 0, 0, st)
+    # host path: rows=None (all rows, range form inside) == explicit list
+    a = pb.entries_estimate(m, v, None, p)
+    b = pb.entries_estimate(m, v, np.arange(csr.n, dtype=np.uint32), p)
+    assert np.array_equal(a.values, b.values) and np.array_equal(a.jumps, b.jumps)
+
+
 def test_results_invariant_to_row_sharding(pb, graphs):
     """Keyed RNG + fixed reduction: any row partition gives identical bits."""
     csr = graphs["ws_3000"]
