@@ -283,8 +283,11 @@ def run_reference(args):
     setup_s = time.perf_counter() - t0
     rows_all = np.arange(rc.n, dtype=np.uint64) if rc.rows is None else \
         rc.rows.astype(np.uint64)
+    # each step a bounded sample, sized so that the whole --steps K --warmup W
+    # run stays within a few minutes (~4 min of sampling)
+    target_s = min(args.cpu_seconds, 240.0 / max(1, args.steps + args.warmup))
     steps, cores, split = cpu_reference_rate(rc.matrix, rc.v, rows_all, rc.walkers, rc.n_steps,
-                                             rc.beta, args.seed, args.cpu_seconds,
+                                             rc.beta, args.seed, target_s,
                                              steps=args.steps, warmup=args.warmup)
     secs = sum(s for s, _, _ in steps)
     jumps = sum(j for _, j, _ in steps)

@@ -1,6 +1,8 @@
-// K3P — pipelined shape of the K3 entry walker (included by walk_entry.cu,
-// inside its anonymous namespace; shares TaskRec, the task stream and the
-// combine pass with entry_walk_kernel).
+// K3P — pipelined two-set shape of the K3 entry walker (included by
+// walk_entry.cu, inside its anonymous namespace; shares TaskRec, the task
+// stream and the combine pass with entry_walk_kernel).  EXPERIMENTAL: selected
+// only by EXPMC_ENTRY_SHAPE=3 (A/B runs and the shape-parity test); measured
+// slower than entry_walk_kernel on every configuration (profiles/r02/README.md).
 //
 // Same random-number and accumulation contract as entry_walk_kernel (gap
 // rounds per (row, part), Philox counters (j, walker, row, 'ENTR'), ticket k
@@ -13,13 +15,13 @@
 //    step of the other set ago; refill idle lanes from the ticket ring; one
 //    jump (Philox, pick, gather) for every lane".  X's gather is in flight
 //    during the whole step of the other set, so each warp keeps two dependent
-//    gathers outstanding instead of one, and the scheduler has two
-//    independent dependency chains per warp.  entry_walk_kernel spends more
-//    than half of each warp's time waiting for its one gather (config 5:
-//    ~2400 of 4400 cycles per iteration).
-//  * The gathered 32-byte Edge lands in shared memory (cp.async, one private
-//    slot per lane and set), not in registers: nothing sits between the load
-//    and its consumer, and a walker in flight costs 12 registers.
+//    gathers outstanding instead of one.
+//  * The gathered 32-byte Edge lands in registers (EPIPE_REGS=1, 87-90
+//    registers, 5 blocks/SM; the slot's unused word is kept live by a store to
+//    the sink slot — otherwise ptxas reuses its register right behind the load
+//    and that write waits for the gather), or in shared memory by cp.async
+//    (EPIPE_REGS=0, 76 registers, 6 blocks/SM; 14 shared-memory wavefronts per
+//    gather instruction put the LSU data pipe at 70%).
 //  * A finishing walker forms its deviation e^{Δt(S − corr)} v_end − K on the
 //    spot and parks only that (8 B over its ticket) plus its jump count, so
 //    the ticket ring is 12 B per ticket and the accumulation pass is a load
@@ -29,6 +31,13 @@
 //    of finished tickets (A).  Admission and the ready-ticket bound (a
 //    min-reduction over the walkers in flight) run once per phase; walkers
 //    stay in their lanes across phases.
+//
+// Why it loses: with 20-24 warps per SM instead of 32 the issue rate falls with
+// the warp count — each warp's instruction stream is a serial dependency chain
+// (stall reason `wait` ~2.7 warps per issue at every occupancy), and running
+// two walkers' streams back to back in one warp adds no instruction-level
+// parallelism.  Config 5: 54.0 ms (registers) / 50.1 ms (cp.async) against
+// 43.7 ms; config 4: 3.27 s against 2.63 s.
 #pragma once
 
 #ifndef EPIPE_CAP
