@@ -75,6 +75,12 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef ENTRY_TAB_SHARED
 #define ENTRY_TAB_SHARED 1 // exp table in shared memory (8-block shape)
 #endif
+#ifndef ENTRY_LONG_WALK
+#define ENTRY_LONG_WALK 8.0
+#endif
+#ifndef ENTRY_GATE_MASK
+#define ENTRY_GATE_MASK 7 // long walks: ready-ticket bound every 8th trip (cfg4: 0 -> 2628, 1 -> 2648, 3 -> 2597, 7 -> 2577 ms)
+#endif
 #ifndef ENTRY_POP_MIN
 #define ENTRY_POP_MIN 4 // run the scheduler once this many lanes are idle (1: cfg4 +4%, 8: cfg4 +13%)
 #endif
@@ -156,7 +162,7 @@ struct WarpState {
 // tasks remain (ring capacity) [4] jumping lanes [5] active lanes
 #endif
 
-template <int WPR, int BL>
+template <int WPR, int BL, int GM = 0>
 __global__ void __launch_bounds__(128, BL)
 entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rate,
                   const Edge* __restrict__ adj, const uint32_t* __restrict__ thr,
@@ -406,6 +412,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         __syncwarp();
     };
 
+    uint32_t trip = 0;
     while (true) {
         // ---- one jump for every walker in flight.  The trip runs jump ->
         // accumulate / finalize -> sojourn -> admit / pop, so the gather issued
@@ -437,6 +444,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         // tstart mod 32) and finalize completed tasks, oldest first.  Tickets
         // [xc, xc + rdy) are popped and finished: the oldest ticket still
         // walking (or the first not popped) bounds them.
+        // (long walks, GM = 2^k - 1: a look every 2^k trips — a walker takes
+        // tens of trips, finished tickets can wait a few more)
+        if (GM == 0 || ((++trip) & (uint32_t)GM) == 0u) {
         const uint32_t minoff = __reduce_min_sync(FULL, act ? tk - xc : ~0u);
         uint32_t rdy = head - xc < minoff ? head - xc : minoff;
         if (rdy >= 32u || (ocl && rdy >= oend - xc)) {
@@ -509,6 +519,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         }
         }
         if (tf == tw && !aopen && atask >= ntask) break;  // every task finalized
+        }
         // ---- sojourn of every walker in flight, at the state just gathered
         bool fin = false, jmp = false;
         if (act) {
@@ -723,6 +734,11 @@ int launch_w(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const Fast
             return launch_t<WPR, entry_pipe_kernel<WPR, EPIPE_BL>, EPIPE_BL>(
                 "entry_pipe_kernel", m, rows, nrows, p, value, se, jumps, partial, s);
         case 0:
+            // long walks (>= ENTRY_LONG_WALK jumps of a walker started at a
+            // random row): ready-ticket look every 8th trip
+            if (p.beta * m.mean_rate >= ENTRY_LONG_WALK)
+                return launch_t<WPR, entry_walk_kernel<WPR, 8, ENTRY_GATE_MASK>, 8>(
+                    "entry_walk_kernel", m, rows, nrows, p, value, se, jumps, partial, s);
             return launch_t<WPR, entry_walk_kernel<WPR, 8>, 8>("entry_walk_kernel", m, rows, nrows,
                                                                p, value, se, jumps, partial, s);
 #ifdef EXPMC_EXPERIMENTS
