@@ -337,3 +337,35 @@ def test_integration_binding_compiles_against_reference(tmp_path):
                         "-I/root/reference/proj/include", "-I" + os.path.join(root, "include"),
                         str(src)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_bench_roofline_levels_and_evidence():
+    """bench.make_roofline: config 5 is judged against the measured HBM peak,
+    the cache-resident configs against the measured L2 gather ceiling
+    (profiles/r02/l2_gather_peak.json); DRAM traffic, sector efficiency and the
+    same-source flag come from the committed ncu captures; the §8d byte model
+    and the design-byte fraction are both present."""
+    import types
+
+    sys.path.insert(0, ROOT)
+    import bench
+
+    l2 = bench._load_json("profiles", "r02", "l2_gather_peak.json")
+    assert l2 and l2["gbs_model_64B"] > 6000 and "how" in l2
+    for idx, bound in ((5, "hbm"), (4, "l2"), (1, "l2")):
+        prof = bench._load_json("profiles", "r02", f"ncu_cfg{idx}.json")
+        assert prof and prof["dram_bytes_per_launch"] > 0 and prof["source_sha"]
+        jumps, entries, ms = 3.2e9, 1e7, 44.0
+        r = bench.make_roofline(types.SimpleNamespace(idx=idx), jumps, entries, ms, 1.0)
+        assert r["bound"] == bound and r["unit"] == "GB/s"
+        balg = 64.0 * jumps + 48.0 * entries
+        assert r["algorithmic_bytes_per_launch"] == balg
+        assert abs(r["achieved"] - balg / (ms / 1e3) / 1e9) < 1e-6 * r["achieved"]
+        assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-12
+        assert r["design_bytes_per_launch"] == 32.0 * jumps + 48.0 * entries
+        assert r["traffic"] == prof["dram_bytes_per_launch"]
+        assert r["traffic_same_source"] == (prof["source_sha"] == bench.source_sha())
+        assert "sector_efficiency" in r and "frac_dram_measured" in r
+    # reduced-scale runs do not borrow the full-size capture
+    r = bench.make_roofline(types.SimpleNamespace(idx=5), 1e6, 1e4, 1.0, 0.01)
+    assert r["traffic"] is None
