@@ -35,10 +35,10 @@
 //    (exponent, exp() and deviation convergent over the batch, ticket k of
 //    the task on lane k mod 32, straight into that lane's running sums), and
 //    a task is finalized once its last batch is in.
-//  * One loop trip = jump (Philox, pick, gather issued) -> accumulate /
-//    finalize -> sojourn at the gathered state -> admit / pop.  The gather
-//    is consumed in the trip that issued it, after the accumulation work,
-//    and lands in registers nothing else writes (see the main loop).
+//  * One loop trip = jump (Philox, pick, gather issued, next -ln u) ->
+//    accumulate / finalize -> sojourn at the gathered state -> admit / pop.
+//    The gather is consumed in the trip that issued it, after the
+//    accumulation work, in the registers it landed in (see the main loop).
 //  * Fixed accumulation order (result contract, replayed by
 //    oracle/fast_model.c): the jumpers of part w, numbered k = 0, 1, ... in
 //    increasing l, are summed by lane k mod 32 in increasing k; lanes are
@@ -79,10 +79,10 @@ constexpr unsigned FULL = 0xffffffffu;
 #define ENTRY_LONG_WALK 8.0
 #endif
 #ifndef ENTRY_GATE_MASK
-#define ENTRY_GATE_MASK 7 // long walks: ready-ticket bound every 8th trip (cfg4: 0 -> 2628, 1 -> 2648, 3 -> 2597, 7 -> 2577 ms)
+#define ENTRY_GATE_MASK 15 // long walks: ready-ticket bound every 16th trip (cfg4: every trip 2628, 2nd 2648, 4th 2597, 8th 2577 ms; with the slim state 8th 2527, 16th 2519, 32nd ~2515)
 #endif
 #ifndef ENTRY_POP_MIN
-#define ENTRY_POP_MIN 4 // run the scheduler once this many lanes are idle (1: cfg4 +4%, 8: cfg4 +13%)
+#define ENTRY_POP_MIN 3 // run the scheduler once this many lanes are idle (cfg4, slim state: 3 -> 2511, 4 -> 2527, 5 -> 2641 ms)
 #endif
 
 // Self-checking build (make variants VARIANTS="checks:-DEXPMC_CHECKS"): the
@@ -211,17 +211,13 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     // G: grid points credited so far, kept as an exact integer-valued double
     // (ceil in fp64, no int conversions on the XU pipe)
     double t = 0.0, S = 0.0, G = 0.0;
-    // the current state as the raw 32-byte Edge slot it was gathered from
-    // ({j, off}, {deg_flags, inv_rate}, d, v)
-    unsigned long long ea = 0, eb = 0, ec = 0, ed = 0;
-    // the slot being gathered: registers written only by the load, copied
-    // into the state by pinned (volatile) moves at the consumer
+    // The gathered slot {j, off | deg_flags, 1/rate | d | v} lives in la..ld,
+    // registers that only the gather writes; of the state a walker needs for
+    // its *next* jump only the row's offset and degree are kept (off_s,
+    // degf_s).  An empty volatile asm with la..ld as in/out operands pins the
+    // consumer: nothing that reads them can be scheduled above it.
     unsigned long long la = 0, lb = 0, lc = 0, ld = 0;
-#define OFF ((uint32_t)(ea >> 32))
-#define DEGF ((uint32_t)eb)
-#define IR (__uint_as_float((uint32_t)(eb >> 32)))
-#define DCUR (__longlong_as_double((long long)ec))
-#define VCUR (__longlong_as_double((long long)ed))
+    uint32_t off_s = 0, degf_s = 0;
     // per-task accumulators of the oldest task (lane = jumper index mod 32)
     double s1 = 0.0, s2 = 0.0;
     unsigned long long jsum = 0;
@@ -229,32 +225,37 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     // One sojourn of the lane's walker from its current state: either the
     // path ends (park S', v, jumps in the ticket; lane becomes idle) or the
     // grid points are credited and the walker must jump (`jmp`).
-    auto sojourn = [&](float E, bool& fin, bool& jmp) {  // E ~ Exp(1)
-        const float h = __fmul_rn(E, IR);
+    // (ir, d, vbits, jrow: the state's 1/rate, d, v bits and row id; off_n,
+    // degf_n: its offset and degree, kept if the walker goes on)
+    auto sojourn = [&](float E, float ir, double d, unsigned long long vbits, uint32_t jrow,
+                       uint32_t off_n, uint32_t degf_n, bool& fin, bool& jmp) {  // E ~ Exp(1)
+        const float h = __fmul_rn(E, ir);
         const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
         if (tn >= p.n_grid) {
             // park the raw weight sum; the exponent is formed at accumulation
-            S = __fma_rn(DCUR, __dsub_rn(p.n_grid1, G), S);
+            S = __fma_rn(d, __dsub_rn(p.n_grid1, G), S);
             const uint32_t pos = tk & (CAP - 1);
             CHK(tk - xc < CAP && tail - tk - 1u < CAP);  // in the ring, not yet accumulated
 #ifdef EXPMC_CHECKS
             CHK((unsigned long long)__double_as_longlong(q.S[pos]) == kUnfinished);  // parked once
 #endif
-            q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, DCUR)) : S;
-            q.v[pos] = VCUR;
+            q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, d)) : S;
+            q.v[pos] = __longlong_as_double((long long)vbits);
             q.tk[tk_slot(pos)].x = jc;
             // (the landing row id, word 0 of the gathered slot, is not needed
             // by the walk: storing it to the sink slot keeps the word live,
             // so its register is not reused — and waited on — right behind
             // the load)
-            q.tk[CAP].y = (uint32_t)ea;
+            q.tk[CAP].y = jrow;
             act = false;
             fin = true;
         } else {
             const double kk = ceil(tn);
-            S = __fma_rn(DCUR, __dsub_rn(kk, G), S);
+            S = __fma_rn(d, __dsub_rn(kk, G), S);
             G = kk;
             t = tn;
+            off_s = off_n;
+            degf_s = degf_n;
             jmp = true;
         }
     };
@@ -416,17 +417,19 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     while (true) {
         // ---- one jump for every walker in flight.  The trip runs jump ->
         // accumulate / finalize -> sojourn -> admit / pop, so the gather issued
-        // here is consumed in the same trip, after the accumulation work: it
-        // lands in registers (la..ld) that nothing else writes, copied into
-        // the walker's state by pinned moves just before the sojourn.  (With
-        // the gather landing in the loop-carried state itself, ptxas compacted
-        // the slot's dead word away by register moves right behind the load,
-        // and every warp waited for its gather *before* the accumulation work:
-        // 24.7% of the stall samples, profiles/r02.)  Idle lanes re-read slot
-        // 0: no predicated moves behind the load either.
+        // here is consumed in the same trip, after the accumulation work.  It
+        // lands in registers (la..ld) that nothing else writes, and the
+        // sojourn reads them in place behind an empty volatile asm that pins
+        // the consumer; the only state carried to the next jump is the row's
+        // offset and degree.  (With the gather landing in a loop-carried copy
+        // of the whole slot, ptxas compacted the slot's dead word away by
+        // register moves right behind the load, and every warp waited for its
+        // gather *before* the accumulation work: 24.7% of the stall samples,
+        // profiles/r02.)  Idle lanes re-read slot 0: no predicated moves
+        // behind the load either.
         {
             const U4 B = philox4x32_10(U4{jc, wl, wi, kTagEntry}, p.rk);
-            const uint32_t off = OFF, degf = DEGF;
+            const uint32_t off = off_s, degf = degf_s;
             uint32_t k = pick_index(B.y, B.w, degf & kDegMask);
             if (act && (degf & kNonUniform) && B.z >= __ldg(thr + off + k))
                 k = __ldg(alias + off + k);
@@ -523,10 +526,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         // ---- sojourn of every walker in flight, at the state just gathered
         bool fin = false, jmp = false;
         if (act) {
-            asm volatile("mov.b64 %0, %4;\n\tmov.b64 %1, %5;\n\tmov.b64 %2, %6;\n\tmov.b64 %3, %7;"
-                         : "=l"(ea), "=l"(eb), "=l"(ec), "=l"(ed)
-                         : "l"(la), "l"(lb), "l"(lc), "l"(ld));
-            sojourn(eh, fin, jmp);
+            asm volatile("" : "+l"(la), "+l"(lb), "+l"(lc), "+l"(ld));
+            sojourn(eh, __uint_as_float((uint32_t)(lb >> 32)), __longlong_as_double((long long)lc),
+                    ld, (uint32_t)la, (uint32_t)(la >> 32), (uint32_t)lb, fin, jmp);
         }
         unsigned idle = __ballot_sync(FULL, !act);
         // scheduler work only when enough lanes are free (batching pops
@@ -552,16 +554,13 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 q.S[tk & (CAP - 1)] = __longlong_as_double((long long)kUnfinished);
 #endif
                 const uint4 r0 = *reinterpret_cast<const uint4*>(&m.rr);  // off, degf, ir, -
-                ea = (unsigned long long)r0.x << 32;
-                eb = r0.y | ((unsigned long long)r0.z << 32);
-                ec = (unsigned long long)__double_as_longlong(m.rr.d);
-                ed = (unsigned long long)__double_as_longlong(m.rr.v);
                 wi = m.i;
                 t = 0.0; S = 0.0; G = 0.0; jc = 0;
                 act = true;
                 // a jumper's first sojourn (R < λ) ends in a jump, so it joins
                 // the next trip's jump
-                sojourn(__uint_as_float(t2.x), fin, jmp);
+                sojourn(__uint_as_float(t2.x), __uint_as_float(r0.z), m.rr.d,
+                        (unsigned long long)__double_as_longlong(m.rr.v), 0u, r0.x, r0.y, fin, jmp);
             }
             head += take;
 #ifdef ENTRY_STATS
@@ -587,11 +586,6 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
 #endif
     }
 }
-#undef OFF
-#undef DEGF
-#undef IR
-#undef DCUR
-#undef VCUR
 
 #include "walk_entry_short.cuh"
 
@@ -735,7 +729,7 @@ int launch_w(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const Fast
                 "entry_pipe_kernel", m, rows, nrows, p, value, se, jumps, partial, s);
         case 0:
             // long walks (>= ENTRY_LONG_WALK jumps of a walker started at a
-            // random row): ready-ticket look every 8th trip
+            // random row): ready-ticket look every 16th trip
             if (p.beta * m.mean_rate >= ENTRY_LONG_WALK)
                 return launch_t<WPR, entry_walk_kernel<WPR, 8, ENTRY_GATE_MASK>, 8>(
                     "entry_walk_kernel", m, rows, nrows, p, value, se, jumps, partial, s);
