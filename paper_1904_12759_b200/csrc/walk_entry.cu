@@ -425,8 +425,8 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         // of the whole slot, ptxas compacted the slot's dead word away by
         // register moves right behind the load, and every warp waited for its
         // gather *before* the accumulation work: 24.7% of the stall samples,
-        // profiles/r02.)  Idle lanes re-read slot 0: no predicated moves
-        // behind the load either.
+        // profiles/r02.)  Idle lanes gather too (a stale slot): no predicate
+        // on the load or behind it.
         {
             const U4 B = philox4x32_10(U4{jc, wl, wi, kTagEntry}, p.rk);
             const uint32_t off = off_s, degf = degf_s;
@@ -434,10 +434,15 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             if (act && (degf & kNonUniform) && B.z >= __ldg(thr + off + k))
                 k = __ldg(alias + off + k);
 #ifdef EXPMC_CHECKS
-            CHK(!act || ((degf & kDegMask) != 0u && k < (degf & kDegMask) &&
-                         (uint64_t)off + k < (uint64_t)(uintptr_t)p.stats));  // p.stats: nnz
+            CHK(!act || ((degf & kDegMask) != 0u && k < (degf & kDegMask)));
+            // every lane gathers (idle lanes a stale but valid slot); p.stats: nnz
+            CHK((uint64_t)(uintptr_t)p.stats == 0 ||
+                (uint64_t)off + k < (uint64_t)(uintptr_t)p.stats);
 #endif
-            ld256_gather(adj + (act ? off + k : 0u), la, lb, lc, ld);
+            // (an idle lane's (off_s, degf_s) are those of a row some walker
+            // stood on — or (0, 0) at the start — so off + k is a valid slot:
+            // no select on the address)
+            ld256_gather(adj + (off + k), la, lb, lc, ld);
             // the next holding-time variate, drawn here so that its polynomial
             // runs under the gather's latency instead of after the wait
             eh = neg_ln_u(B.x);
