@@ -535,11 +535,10 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             sojourn(eh, __uint_as_float((uint32_t)(lb >> 32)), __longlong_as_double((long long)lc),
                     ld, (uint32_t)la, (uint32_t)(la >> 32), (uint32_t)lb, fin, jmp);
         }
-        unsigned idle = __ballot_sync(FULL, !act);
+        const unsigned idle = __ballot_sync(FULL, !act);
         // scheduler work only when enough lanes are free (batching pops
         // amortises the scheduler over several walkers)
-        if (__popc(idle) < ENTRY_POP_MIN && idle != FULL) idle = 0;
-        if (idle) {
+        if (__popc(idle) >= ENTRY_POP_MIN) {
             // ---- admit: sweep chunks while queued tickets cannot feed the
             // idle lanes and a whole chunk's tickets fit in the ring
             while (can_admit() && tail - head < (uint32_t)__popc(idle)) admit();
@@ -547,6 +546,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             const uint32_t avail = tail - head;
             const uint32_t nidle = (uint32_t)__popc(idle);
             const uint32_t take = avail < nidle ? avail : nidle;
+            // lanes left without tickets (ring or task slots held by work
+            // that awaits accumulation): look at the next trip, not the 16th
+            if (GM != 0 && avail < nidle) trip = (uint32_t)GM;
             const uint32_t rank = (uint32_t)__popc(idle & lt);
             if (!act && rank < take) {
                 tk = head + rank;
@@ -735,7 +737,9 @@ int launch_w(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const Fast
         case 0:
             // long walks (>= ENTRY_LONG_WALK jumps of a walker started at a
             // random row): ready-ticket look every 16th trip
-            if (p.beta * m.mean_rate >= ENTRY_LONG_WALK)
+            // (and enough walkers per task that task slots do not wait on
+            // the look: measured 8-20% slower at 16-64 walkers per entry)
+            if (p.beta * m.mean_rate >= ENTRY_LONG_WALK && p.W / WPR >= 512)
                 return launch_t<WPR, entry_walk_kernel<WPR, 8, ENTRY_GATE_MASK>, 8>(
                     "entry_walk_kernel", m, rows, nrows, p, value, se, jumps, partial, s);
             return launch_t<WPR, entry_walk_kernel<WPR, 8>, 8>("entry_walk_kernel", m, rows, nrows,
