@@ -76,7 +76,7 @@ constexpr unsigned FULL = 0xffffffffu;
 #define ENTRY_TAB_SHARED 1 // exp table in shared memory (8-block shape)
 #endif
 #ifndef ENTRY_LONG_WALK
-#define ENTRY_LONG_WALK 8.0
+#define ENTRY_LONG_WALK 8.0 // mean jumps per walker (β · mean rate) from which the long-walk gate applies
 #endif
 #ifndef ENTRY_GATE_MASK
 #define ENTRY_GATE_MASK 15 // long walks: ready-ticket bound every 16th trip (cfg4: every trip 2628, 2nd 2648, 4th 2597, 8th 2577 ms; with the slim state 8th 2527, 16th 2519, 32nd ~2515)
@@ -152,9 +152,8 @@ struct WarpState {
     uint2 tk[CAP + 1];  // per ticket: {first holding time R·rate (fp32) until popped,
                         //   then the jump count; task slot << 29 | walker l}; the
                         //   last is the sink of the sweep's unconditional stores
-                        //   (7 blocks x (smem + 1 KB) must stay under the 196 KB
-                        //   carveout: 1 KB more moved config 4 to a 28 KB L1 and
-                        //   1.86x the time)
+                        //   (4 warps x 6800 B + the 512-B exp table: 8 blocks per
+                        //   SM under the 228 KB carveout)
 };
 
 #ifdef ENTRY_STATS

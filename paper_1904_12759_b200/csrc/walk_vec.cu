@@ -332,11 +332,18 @@ vec_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj,
     double s1 = 0.0, s2 = 0.0;
     unsigned long long jt = 0;
     bool active = false;
-    uint32_t i = 0, cur = 0, off = 0, degf = 0, step = 0, jc = 0, klo = 0, tagv = 0;
-    float ir = 0.f;
-    double dcur = 0.0, t = 0.0, S = 0.0, g = 0.0, corr0 = 0.0;
+    uint32_t i = 0, off = 0, degf = 0, step = 0, jc = 0, klo = 0, tagv = 0;
+    uint32_t wy = 0, ww = 0, wz = 0;  // Philox words of the walker's next jump
+    double t = 0.0, S = 0.0, g = 0.0, corr0 = 0.0;
     // start row of the lane's next jumper, loaded one walker ahead
     uint32_t inext = q < q1 ? __ldg(row_of + (q - q0)) : 0u;
+    // One trip = (start of the lane's next walker if it has none) -> jump ->
+    // Philox block and -ln u of the next step -> sojourn at the landing state.
+    // The gathered slot is consumed in the trip that issued it, with the next
+    // step's Philox and logarithm between the load and its first use.  (With
+    // the landing state carried across the back edge instead, ptxas copies
+    // loaded registers right behind the load and the lane waits for the
+    // gather at once — the pattern found in K3, profiles/r02/README.md.)
     while (true) {
         if (!active) {
             if (q >= q1) break;
@@ -359,39 +366,45 @@ vec_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ adj,
             S = __dmul_rn(rs.d, kk);
             g = kk;
             t = tn;
-            const Edge e = jump_edge(w.y, w.w, w.z, rs.off, rs.deg_flags, adj, thr, alias);
-            cur = e.j; off = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d;
-            jc = 1;
-            step = 1;
+            off = rs.off;
+            degf = rs.deg_flags;
+            wy = w.y; ww = w.w; wz = w.z;
+            jc = 0;
+            step = 0;
             active = true;
         }
+        // the jump drawn at the previous step (or at the start) ...
+        const Edge e = jump_edge(wy, ww, wz, off, degf, adj, thr, alias);
+        ++jc;
+        ++step;
+        // ... and, under its gather, this step's Philox block and variate
         const U4 w = philox4x32_10(U4{step, klo, 0u, tagv}, p.rk);
-        const float h = __fmul_rn(neg_ln_u(w.x), ir);
+        const float E = neg_ln_u(w.x);
+        const float h = __fmul_rn(E, e.inv_rate);
         const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
         if (tn >= p.n_grid) {
-            S = __fma_rn(dcur, __dsub_rn(p.n_grid1, g), S);
-            const double corr = p.strang ? __dadd_rn(corr0, __dmul_rn(0.5, dcur)) : dcur;
+            S = __fma_rn(e.d, __dsub_rn(p.n_grid1, g), S);
+            const double corr = p.strang ? __dadd_rn(corr0, __dmul_rn(0.5, e.d)) : e.d;
             const double f = __dmul_rn(v_sum, exp(__dmul_rn(p.dt, __dsub_rn(S, corr))));
             s1 = __dadd_rn(s1, f);
             s2 = __fma_rn(f, f, s2);
             jt += jc;
             if (acc) {
-                fixed_add(acc, cur, f, scale_hi);
+                fixed_add(acc, e.j, f, scale_hi);
             } else if (out_end) {
-                out_end[q - q0] = cur;
+                out_end[q - q0] = e.j;
                 out_f[q - q0] = f;
             }
             active = false;
             q += stride;
         } else {
             const double kk = ceil(tn);
-            S = __fma_rn(dcur, __dsub_rn(kk, g), S);
+            S = __fma_rn(e.d, __dsub_rn(kk, g), S);
             g = kk;
             t = tn;
-            const Edge e = jump_edge(w.y, w.w, w.z, off, degf, adj, thr, alias);
-            cur = e.j; off = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d;
-            ++jc;
-            ++step;
+            off = e.off;
+            degf = e.deg_flags;
+            wy = w.y; ww = w.w; wz = w.z;
         }
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -480,10 +493,11 @@ entry_big_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ a
     q1 = qend;
     bool active = false;
     uint32_t r = 0, i = 0, off_c = 0, degf = 0, step = 0, jc = 0, klo = 0, tagv = 0;
-    float ir = 0.f;
-    double dcur = 0.0, vcur = 0.0, t = 0.0, S = 0.0, g = 0.0, corr0 = 0.0, K = 0.0;
+    uint32_t wy = 0, ww = 0, wz = 0;  // Philox words of the walker's next jump
+    double t = 0.0, S = 0.0, g = 0.0, corr0 = 0.0, K = 0.0;
     uint32_t ar = 0xffffffffu;  // row of the lane's open jump count
     unsigned long long aj = 0;
+    // trip order as vec_walk_kernel: start -> jump -> next Philox / -ln u -> sojourn
     while (true) {
         if (!active) {
             if (q >= q1) break;
@@ -510,21 +524,26 @@ entry_big_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ a
             S = __dmul_rn(rs.d, kk);
             g = kk;
             t = tn;
-            const Edge e = jump_edge(w.y, w.w, w.z, rs.off, rs.deg_flags, adj, thr, alias);
-            off_c = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d; vcur = e.v;
-            jc = 1;
-            step = 1;
+            off_c = rs.off;
+            degf = rs.deg_flags;
+            wy = w.y; ww = w.w; wz = w.z;
+            jc = 0;
+            step = 0;
             active = true;
         }
+        const Edge e = jump_edge(wy, ww, wz, off_c, degf, adj, thr, alias);
+        ++jc;
+        ++step;
         const U4 w = philox4x32_10(U4{step, klo, i, tagv}, p.rk);
-        const float h = __fmul_rn(neg_ln_u(w.x), ir);
+        const float E = neg_ln_u(w.x);
+        const float h = __fmul_rn(E, e.inv_rate);
         const double tn = __dadd_rn(t, __dmul_rn((double)h, p.inv_dt));
         if (tn >= p.n_grid) {
-            S = __fma_rn(dcur, __dsub_rn(p.n_grid1, g), S);
+            S = __fma_rn(e.d, __dsub_rn(p.n_grid1, g), S);
             // Strang: half weights at both ends; Lie: after-weights only
             // (estimator.cpp:176-180) — K3's exponent
-            const double Sx = p.strang ? __dsub_rn(S, __dmul_rn(0.5, dcur)) : S;
-            const double f = __dmul_rn(exp(__dmul_rn(p.dt, __dsub_rn(Sx, corr0))), vcur);
+            const double Sx = p.strang ? __dsub_rn(S, __dmul_rn(0.5, e.d)) : S;
+            const double f = __dmul_rn(exp(__dmul_rn(p.dt, __dsub_rn(Sx, corr0))), e.v);
             const double dv = __dsub_rn(f, K);
             dev1[q - q0] = dv;
             dev2[q - q0] = __dmul_rn(dv, dv);
@@ -533,13 +552,12 @@ entry_big_walk_kernel(const RowRec* __restrict__ rec, const Edge* __restrict__ a
             q += stride;
         } else {
             const double kk = ceil(tn);
-            S = __fma_rn(dcur, __dsub_rn(kk, g), S);
+            S = __fma_rn(e.d, __dsub_rn(kk, g), S);
             g = kk;
             t = tn;
-            const Edge e = jump_edge(w.y, w.w, w.z, off_c, degf, adj, thr, alias);
-            off_c = e.off; degf = e.deg_flags; ir = e.inv_rate; dcur = e.d; vcur = e.v;
-            ++jc;
-            ++step;
+            off_c = e.off;
+            degf = e.deg_flags;
+            wy = w.y; ww = w.w; wz = w.z;
         }
     }
     if (ar != 0xffffffffu && aj) atomicAdd(jumps + ar, aj);
