@@ -246,15 +246,15 @@ void finish_split(expmc_matrix* h) {
     DevSplit& m = h->m;
     const uint64_t n = m.n, nnz = m.nnz;
     cudaStream_t s = h->stream;
-    unsigned long long* sc = h->scal.get<unsigned long long>(4);
-    const unsigned long long init[4] = {~0ull, 0ull, 0ull, 0ull};
+    unsigned long long* sc = h->scal.get<unsigned long long>(8);
+    const unsigned long long init[5] = {~0ull, 0ull, 0ull, 0ull, 0ull};
     CK(cudaMemcpyAsync(sc, init, sizeof(init), cudaMemcpyHostToDevice, s));
     launch_split_pack(n, m.row_offset, m.weight, m.diag, m.d, m.rate, m.cum, m.uniform_row, m.rec,
                       sc + 1, reinterpret_cast<unsigned int*>(sc + 2), s);
     after_launch(n ? 1 : 0);
-    launch_rate_sum(n, m.rate, reinterpret_cast<double*>(sc + 3), s);
+    launch_rate_sum(n, m.rate, m.d, reinterpret_cast<double*>(sc + 3), sc + 4, s);
     after_launch(n ? 1 : 0);
-    unsigned long long res[4];
+    unsigned long long res[5];
     CK(cudaMemcpyAsync(res, sc, sizeof(res), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     m.dmax = res[1];
@@ -264,6 +264,7 @@ void finish_split(expmc_matrix* h) {
         double rs;
         std::memcpy(&rs, &res[3], 8);
         m.mean_rate = n > 0 ? rs / (double)n : 0.0;
+        std::memcpy(&m.dabs_max, &res[4], 8);
     }
     if (m.any_nonuniform) {
         m.alias_thr = h->alloc<uint32_t>(nnz);

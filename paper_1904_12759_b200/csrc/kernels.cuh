@@ -25,6 +25,7 @@ struct DevSplit {
     uint64_t dmax = 0;
     bool any_nonuniform = false;
     double mean_rate = 0.0;      // launch heuristics only (K3 occupancy choice)
+    double dabs_max = 0.0;       // max |d_i| (+inf if some d is not finite): K3's exp range bound
     // walk layout
     RowRec* rec = nullptr;       // n packed 32-B row records
     uint32_t* alias_thr = nullptr; // nnz (only if any_nonuniform)
@@ -49,6 +50,8 @@ struct FastParams {
     PhiloxKeys rk;
     unsigned long long* stats = nullptr;  // ENTRY_STATS builds only
     uint32_t row0 = 0;  // K3 with rows == nullptr: the launch covers rows [row0, row0 + nrows)
+    int exp_safe = 0;   // K3: every exponent Δt (S - corr) is within ±690 (set per launch
+                        // from max |d|): exp_det without range clamps, same bits
 };
 
 // split_pack.cu
@@ -58,7 +61,8 @@ void launch_split_pack(uint64_t n, const uint64_t* row_ptr, const double* weight
                        const double* diag, double* d, double* rate, double* cum,
                        uint8_t* uniform_row, RowRec* rec, unsigned long long* dmax,
                        unsigned int* any_nonuniform, cudaStream_t s);
-void launch_rate_sum(uint64_t n, const double* rate, double* out, cudaStream_t s);
+void launch_rate_sum(uint64_t n, const double* rate, const double* d, double* out,
+                     unsigned long long* dabs_max, cudaStream_t s);
 void launch_alias_build(uint64_t n, const uint64_t* row_ptr, const double* weight,
                         const double* rate, const uint8_t* uniform_row, uint32_t* thr,
                         uint32_t* alias, double* p, uint32_t* small, uint32_t* large,

@@ -221,21 +221,39 @@ void launch_split_pack(uint64_t n, const uint64_t* row_ptr, const double* weight
 }
 
 // Sum of the row rates (launch heuristics only: per-warp atomics, so the
-// last bits depend on the schedule; never feeds a result).
+// last bits depend on the schedule; never feeds a result) and max |d_i| (the
+// bound that lets K3 drop exp_det's range clamps: exact, order-independent).
 __global__ void rate_sum_kernel(uint64_t n, const double* __restrict__ rate,
-                                double* __restrict__ out) {
-    double acc = 0.0;
+                                const double* __restrict__ d, double* __restrict__ out,
+                                unsigned long long* __restrict__ dabs_max) {
+    double acc = 0.0, mx = 0.0;
+    bool bad = false;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
+         i += (uint64_t)gridDim.x * blockDim.x) {
         acc += rate[i];
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+        const double a = fabs(d[i]);
+        bad = bad || !(a <= 1.7976931348623157e308);  // NaN / inf: no bound
+        mx = a > mx ? a : mx;
+    }
+    if (bad) mx = __longlong_as_double(0x7ff0000000000000ll);
+    for (int o = 16; o > 0; o >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        const double y = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = y > mx ? y : mx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out, acc);
+        // non-negative doubles order like their bit patterns
+        atomicMax(dabs_max, (unsigned long long)__double_as_longlong(mx));
+    }
 }
 
-void launch_rate_sum(uint64_t n, const double* rate, double* out, cudaStream_t s) {
+void launch_rate_sum(uint64_t n, const double* rate, const double* d, double* out,
+                     unsigned long long* dabs_max, cudaStream_t s) {
     if (n == 0) return;
     const uint64_t want = (n + 255) / 256;
-    rate_sum_kernel<<<(unsigned)(want < 1184 ? want : 1184), 256, 0, s>>>(n, rate, out);
+    rate_sum_kernel<<<(unsigned)(want < 1184 ? want : 1184), 256, 0, s>>>(n, rate, d, out,
+                                                                         dabs_max);
 }
 
 void launch_alias_build(uint64_t n, const uint64_t* row_ptr, const double* weight,

@@ -81,6 +81,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef ENTRY_GATE_MASK
 #define ENTRY_GATE_MASK 15 // long walks: ready-ticket bound every 16th trip (cfg4: every trip 2628, 2nd 2648, 4th 2597, 8th 2577 ms; with the slim state 8th 2527, 16th 2519, 32nd ~2515)
 #endif
+#ifndef ENTRY_EXP_INRANGE
+#define ENTRY_EXP_INRANGE 1 // clamp-free exp_det when the launch's exponents are provably within range
+#endif
 #ifndef ENTRY_POP_MIN
 #define ENTRY_POP_MIN 3 // run the scheduler once this many lanes are idle (cfg4, slim state: 3 -> 2511, 4 -> 2527, 5 -> 2641 ms)
 #endif
@@ -480,9 +483,11 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                     CHK((q.tk[tk_slot(pos)].y >> 29) == (tf & (RT - 1)));  // ...and is this task's
 #endif
                     const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], m.corr));
-                    const double dv = __dsub_rn(
-                        __dmul_rn(kTabShared ? exp_det_tab(x, s_tab, false) : exp_det(x), q.v[pos]),
-                        m.K);
+                    // (p.exp_safe: |x| <= 690 for every walker of this launch)
+                    const double ex = !kTabShared ? exp_det(x)
+                                      : p.exp_safe ? exp_det_inrange(x, s_tab)
+                                                   : exp_det_tab(x, s_tab, false);
+                    const double dv = __dsub_rn(__dmul_rn(ex, q.v[pos]), m.K);
                     s1 = __dadd_rn(s1, dv);
                     s2 = __fma_rn(dv, dv, s2);
                     jsum += q.tk[tk_slot(pos)].x;
@@ -771,9 +776,14 @@ size_t entry_fast_scratch_bytes(uint64_t nrows, uint64_t W) {
 }
 
 int launch_entry_fast(const DevSplit& m, const uint32_t* rows, uint64_t nrows,
-                      const FastParams& p, double* value, double* se, uint64_t* jumps,
+                      const FastParams& p_in, double* value, double* se, uint64_t* jumps,
                       void* scratch, cudaStream_t s) {
     if (nrows == 0) return 0;
+    // Every exponent a walker forms is Δt (S - corr) with |S| <= (N + 1) max|d|
+    // and |corr| <= max|d|: inside ±690 when β max|d| (N + 2) / N is.
+    FastParams p = p_in;
+    p.exp_safe = ENTRY_EXP_INRANGE &&
+                 p.beta * m.dabs_max * ((double)p.N + 2.0) / (double)p.N < 690.0;
     double4* part = static_cast<double4*>(scratch);
 #ifdef ENTRY_STATS
     static unsigned long long* st = nullptr;
