@@ -84,6 +84,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef ENTRY_EXP_INRANGE
 #define ENTRY_EXP_INRANGE 1 // clamp-free exp_det when the launch's exponents are provably within range
 #endif
+#ifndef ENTRY_EXIT_AT_FINALIZE
+#define ENTRY_EXIT_AT_FINALIZE 0 // 1: the kernel's exit test runs after a finalize only, not every trip
+#endif
 #ifndef ENTRY_POP_MIN
 #define ENTRY_POP_MIN 3 // run the scheduler once this many lanes are idle (cfg4, slim state: 3 -> 2511, 4 -> 2527, 5 -> 2641 ms)
 #endif
@@ -416,6 +419,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     };
 
     uint32_t trip = 0;
+#if ENTRY_EXIT_AT_FINALIZE
+    if (atask >= ntask) return;  // a warp without a task
+#endif
     while (true) {
         // ---- one jump for every walker in flight.  The trip runs jump ->
         // accumulate / finalize -> sojourn -> admit / pop, so the gather issued
@@ -459,42 +465,35 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         if (GM == 0 || ((++trip) & (uint32_t)GM) == 0u) {
         const uint32_t minoff = __reduce_min_sync(FULL, act ? tk - xc : ~0u);
         uint32_t rdy = head - xc < minoff ? head - xc : minoff;
+        // (entry / continuation test: a full batch is ready, or every
+        // remaining ticket of the closed oldest task is; it implies tf != tw)
         if (rdy >= 32u || (ocl && rdy >= oend - xc)) {
         __syncwarp();
-        while (tf != tw) {
+        do {
             const TaskRec& m = q.task[tf & (RT - 1)];
-            // ready tickets of this task (offsets from xc)
-            const uint32_t lim = ocl && oend - xc < rdy ? oend - xc : rdy;
-            uint32_t nb;
-            if (lim >= 32u) {
-                nb = 32u;                     // a full batch
-            } else if (ocl && lim == oend - xc) {
-                nb = lim;                     // the closed task's last (partial) batch
-            } else {
-                break;                        // wait for more tickets
-            }
-            if (nb) {
-                CHK(xc + nb - xc <= head - xc && nb <= 32u);
-                if ((uint32_t)lane < nb) {
-                    const uint32_t pos = (xc + lane) & (CAP - 1);
+            // a full batch, or the closed task's last (possibly empty) one
+            const uint32_t rem = oend - xc;
+            const uint32_t nb = ocl && rdy >= rem && rem < 32u ? rem : 32u;
+            CHK(tf != tw && nb <= head - xc && nb <= rdy);
+            if ((uint32_t)lane < nb) {
+                const uint32_t pos = (xc + lane) & (CAP - 1);
 #ifdef EXPMC_CHECKS
-                    // every ticket of the batch was popped and parked
-                    CHK((unsigned long long)__double_as_longlong(q.S[pos]) != kUnfinished);
-                    CHK((q.tk[tk_slot(pos)].y >> 29) == (tf & (RT - 1)));  // ...and is this task's
+                // every ticket of the batch was popped and parked
+                CHK((unsigned long long)__double_as_longlong(q.S[pos]) != kUnfinished);
+                CHK((q.tk[tk_slot(pos)].y >> 29) == (tf & (RT - 1)));  // ...and is this task's
 #endif
-                    const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], m.corr));
-                    // (p.exp_safe: |x| <= 690 for every walker of this launch)
-                    const double ex = !kTabShared ? exp_det(x)
-                                      : p.exp_safe ? exp_det_inrange(x, s_tab)
-                                                   : exp_det_tab(x, s_tab, false);
-                    const double dv = __dsub_rn(__dmul_rn(ex, q.v[pos]), m.K);
-                    s1 = __dadd_rn(s1, dv);
-                    s2 = __fma_rn(dv, dv, s2);
-                    jsum += q.tk[tk_slot(pos)].x;
-                }
-                xc += nb;
-                rdy -= nb;
+                const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], m.corr));
+                // (p.exp_safe: |x| <= 690 for every walker of this launch)
+                const double ex = !kTabShared ? exp_det(x)
+                                  : p.exp_safe ? exp_det_inrange(x, s_tab)
+                                               : exp_det_tab(x, s_tab, false);
+                const double dv = __dsub_rn(__dmul_rn(ex, q.v[pos]), m.K);
+                s1 = __dadd_rn(s1, dv);
+                s2 = __fma_rn(dv, dv, s2);
+                jsum += q.tk[tk_slot(pos)].x;
             }
+            xc += nb;
+            rdy -= nb;
             if (!ocl || xc != oend) continue;
             // task complete: butterfly, never-jumpers, output
 #pragma unroll
@@ -528,9 +527,18 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 ocl = e.y != 0u;
                 oend = e.x;
             }
+#if ENTRY_EXIT_AT_FINALIZE
+            // every task finalized (no task is in flight only right after a
+            // finalize, or from the start: checked before the loop)
+            else if (atask >= ntask) {
+                goto finished;
+            }
+#endif
+        } while (rdy >= 32u || (ocl && rdy >= oend - xc));
         }
-        }
+#if !ENTRY_EXIT_AT_FINALIZE
         if (tf == tw && !aopen && atask >= ntask) break;  // every task finalized
+#endif
         }
         // ---- sojourn of every walker in flight, at the state just gathered
         bool fin = false, jmp = false;
@@ -545,7 +553,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         if (__popc(idle) >= ENTRY_POP_MIN) {
             // ---- admit: sweep chunks while queued tickets cannot feed the
             // idle lanes and a whole chunk's tickets fit in the ring
-            while (can_admit() && tail - head < (uint32_t)__popc(idle)) admit();
+            while (tail - head < (uint32_t)__popc(idle) && can_admit()) admit();
             // ---- pop: idle lanes take tickets in order
             const uint32_t avail = tail - head;
             const uint32_t nidle = (uint32_t)__popc(idle);
@@ -596,6 +604,9 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         }
 #endif
     }
+#if ENTRY_EXIT_AT_FINALIZE
+finished:;
+#endif
 }
 
 #include "walk_entry_short.cuh"
