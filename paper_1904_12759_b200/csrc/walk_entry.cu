@@ -84,9 +84,6 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef ENTRY_EXP_INRANGE
 #define ENTRY_EXP_INRANGE 1 // clamp-free exp_det when the launch's exponents are provably within range
 #endif
-#ifndef ENTRY_EXIT_AT_FINALIZE
-#define ENTRY_EXIT_AT_FINALIZE 0 // 1: the kernel's exit test runs after a finalize only, not every trip
-#endif
 #ifndef ENTRY_POP_MIN
 #define ENTRY_POP_MIN 3 // run the scheduler once this many lanes are idle (cfg4, slim state: 3 -> 2511, 4 -> 2527, 5 -> 2641 ms)
 #endif
@@ -167,7 +164,9 @@ struct WarpState {
 // tasks remain (ring capacity) [4] jumping lanes [5] active lanes
 #endif
 
-template <int WPR, int BL, int GM = 0>
+// (WT = false: a matrix without weighted rows — every configuration of the
+// benchmark — needs neither the flag bit nor the alias test in the jump)
+template <int WPR, int BL, int GM = 0, bool WT = true>
 __global__ void __launch_bounds__(128, BL)
 entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rate,
                   const Edge* __restrict__ adj, const uint32_t* __restrict__ thr,
@@ -419,9 +418,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     };
 
     uint32_t trip = 0;
-#if ENTRY_EXIT_AT_FINALIZE
     if (atask >= ntask) return;  // a warp without a task
-#endif
     while (true) {
         // ---- one jump for every walker in flight.  The trip runs jump ->
         // accumulate / finalize -> sojourn -> admit / pop, so the gather issued
@@ -438,10 +435,13 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         {
             const U4 B = philox4x32_10(U4{jc, wl, wi, kTagEntry}, p.rk);
             const uint32_t off = off_s, degf = degf_s;
-            uint32_t k = pick_index(B.y, B.w, degf & kDegMask);
-            if (act && (degf & kNonUniform) && B.z >= __ldg(thr + off + k))
-                k = __ldg(alias + off + k);
+            uint32_t k = pick_index(B.y, B.w, WT ? degf & kDegMask : degf);
+            if (WT) {
+                if (act && (degf & kNonUniform) && B.z >= __ldg(thr + off + k))
+                    k = __ldg(alias + off + k);
+            }
 #ifdef EXPMC_CHECKS
+            CHK(WT || (degf & kNonUniform) == 0u);
             CHK(!act || ((degf & kDegMask) != 0u && k < (degf & kDegMask)));
             // every lane gathers (idle lanes a stale but valid slot); p.stats: nnz
             CHK((uint64_t)(uintptr_t)p.stats == 0 ||
@@ -527,18 +527,14 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 ocl = e.y != 0u;
                 oend = e.x;
             }
-#if ENTRY_EXIT_AT_FINALIZE
-            // every task finalized (no task is in flight only right after a
-            // finalize, or from the start: checked before the loop)
+            // every task finalized: the kernel's exit.  (No task is in flight
+            // only right after a finalize — tested here, not every trip: cfg5
+            // 41.04 -> 40.68 ms — or from the start, tested before the loop.)
             else if (atask >= ntask) {
                 goto finished;
             }
-#endif
         } while (rdy >= 32u || (ocl && rdy >= oend - xc));
         }
-#if !ENTRY_EXIT_AT_FINALIZE
-        if (tf == tw && !aopen && atask >= ntask) break;  // every task finalized
-#endif
         }
         // ---- sojourn of every walker in flight, at the state just gathered
         bool fin = false, jmp = false;
@@ -604,9 +600,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
         }
 #endif
     }
-#if ENTRY_EXIT_AT_FINALIZE
 finished:;
-#endif
 }
 
 #include "walk_entry_short.cuh"
@@ -754,8 +748,15 @@ int launch_w(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const Fast
             // random row): ready-ticket look every 16th trip
             // (and enough walkers per task that task slots do not wait on
             // the look: measured 8-20% slower at 16-64 walkers per entry)
-            if (p.beta * m.mean_rate >= ENTRY_LONG_WALK && p.W / WPR >= 512)
+            if (p.beta * m.mean_rate >= ENTRY_LONG_WALK && p.W / WPR >= 512) {
+                if (!m.any_nonuniform)
+                    return launch_t<WPR, entry_walk_kernel<WPR, 8, ENTRY_GATE_MASK, false>, 8>(
+                        "entry_walk_kernel", m, rows, nrows, p, value, se, jumps, partial, s);
                 return launch_t<WPR, entry_walk_kernel<WPR, 8, ENTRY_GATE_MASK>, 8>(
+                    "entry_walk_kernel", m, rows, nrows, p, value, se, jumps, partial, s);
+            }
+            if (!m.any_nonuniform)
+                return launch_t<WPR, entry_walk_kernel<WPR, 8, 0, false>, 8>(
                     "entry_walk_kernel", m, rows, nrows, p, value, se, jumps, partial, s);
             return launch_t<WPR, entry_walk_kernel<WPR, 8>, 8>("entry_walk_kernel", m, rows, nrows,
                                                                p, value, se, jumps, partial, s);

@@ -108,3 +108,40 @@ def test_concurrent_callers_share_a_handle(pb):
     for k in range(len(vs)):
         for r in range(4):
             assert np.array_equal(got[k][r], want[k])
+
+
+_PIECES_SCRIPT = r"""
+import sys, numpy as np
+import paper_1904_12759_b200 as pb
+csr = pb.gen_ba(20_000, 4, 3)
+v = pb.gen_vector(1, csr.n, 5)
+m = pb.split(csr)
+p = pb.PathParams(0.05, 32, 1000, pb.Splitting.Strang, 9)
+rows = np.random.default_rng(1).choice(csr.n, 5003, replace=False).astype(np.uint32)
+a = pb.entries_estimate(m, v, rows, p)
+b = pb.entries_estimate(m, v, None, p)
+np.savez(sys.argv[1], av=a.values, ase=a.std_errors, aj=a.jumps, at=a.total_jumps,
+         bv=b.values, bse=b.std_errors, bj=b.jumps, bt=b.total_jumps)
+"""
+
+
+def test_host_call_result_pieces_do_not_change_a_bit(tmp_path):
+    """The host entry call walks large requests in pieces (halves, so that
+    only a small last piece's copy-back is exposed: api.cu run_entries); the
+    pieces are a row sharding, so any piece count gives the same bits.
+    EXPMC_PIECES forces the piece path on a small request."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for pieces in ("1", "6", "13"):
+        f = tmp_path / f"p{pieces}.npz"
+        env = dict(os.environ, EXPMC_PIECES=pieces, PYTHONPATH=root)
+        subprocess.run([sys.executable, "-c", _PIECES_SCRIPT, str(f)], check=True, env=env,
+                       cwd=root, timeout=600)
+        out[pieces] = np.load(f)
+    for pieces in ("6", "13"):
+        for k in out["1"].files:
+            assert np.array_equal(out["1"][k], out[pieces][k]), (pieces, k)
