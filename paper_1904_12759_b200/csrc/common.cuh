@@ -148,11 +148,11 @@ constexpr uint32_t kTagScatter = 0x56454354u; // 'VECT' (vector / tc)
 // with the gathers, profiles/r02/README.md.)
 __device__ __forceinline__ float neg_ln_u(uint32_t w) {
     const uint32_t bits = __float_as_uint(__uint2float_rn(w | 1u));
-    int e = (int)(bits >> 23) - 127;
+    int e32 = 159 - (int)(bits >> 23);  // 32 - e
     float m = __uint_as_float((bits & 0x007fffffu) | 0x3f800000u);  // [1,2)
     if (m > 1.41421356f) {
         m = __fmul_rn(m, 0.5f);
-        e += 1;
+        e32 -= 1;
     }
     const float f = __fsub_rn(m, 1.0f);
     float q = 0.08743945509195328f;
@@ -164,7 +164,7 @@ __device__ __forceinline__ float neg_ln_u(uint32_t w) {
     q = __fmaf_rn(q, f, 0.3333418369293213f);
     q = __fmaf_rn(q, f, -0.49999988079071045f);
     q = __fmaf_rn(q, f, 1.0f);
-    const float E = __fmaf_rn(__int2float_rn(32 - e), 0.693147182f, -__fmul_rn(f, q));
+    const float E = __fmaf_rn(__int2float_rn(e32), 0.693147182f, -__fmul_rn(f, q));
     return E > 0.0f ? E : 0.0f;
 }
 
@@ -266,8 +266,8 @@ __device__ __forceinline__ double exp_det_inrange(double x, const double2* __res
 // floor(x * n / 2^64) for a 64-bit uniform x: unbiased to n / 2^64.
 __device__ __forceinline__ uint32_t pick_index(uint32_t hi, uint32_t lo,
                                                uint32_t n) {
-    const uint64_t x = ((uint64_t)hi << 32) | lo;
-    return (uint32_t)__umul64hi(x, (uint64_t)n);
+    // = umul64hi(hi:lo, n): the high word of lo n carries into hi n
+    return (uint32_t)(((uint64_t)hi * n + __umulhi(lo, n)) >> 32);
 }
 
 // One 32-byte row record through the read-only path (2 x 16-B loads of

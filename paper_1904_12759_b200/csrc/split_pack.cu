@@ -170,7 +170,9 @@ __global__ void build_adj_kernel(uint64_t nnz, const uint32_t* __restrict__ neig
 // stride, gathers of v from an L2-resident vector).
 // Per-call refresh of Edge.v: the landing row comes from the 4-byte CSR
 // neighbour array (0.64 GB at config 5) rather than from the 32-byte slots
-// themselves (5.1 GB), so the pass reads 8x less.
+// themselves (5.1 GB), so the pass reads 8x less.  (2.55 ms at config 5;
+// measured no better: streaming ld.cs / st.cs 2.52 ms, whole-slot 256-bit
+// read-modify-write 2.78 ms — profiles/r02/k3_steps.txt, ab_x.)
 __global__ void pack_v_adj_kernel(uint64_t nnz, const uint32_t* __restrict__ neighbor,
                                   const double* __restrict__ v, Edge* __restrict__ adj) {
     const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
