@@ -165,8 +165,12 @@ struct WarpState {
 #endif
 
 // (WT = false: a matrix without weighted rows — every configuration of the
-// benchmark — needs neither the flag bit nor the alias test in the jump)
-template <int WPR, int BL, int GM = 0, bool WT = true>
+// benchmark — needs neither the flag bit nor the alias test in the jump.
+// SPL = 0 / 1: the splitting (Lie / Strang) known at compile time, -1: read
+// from the parameters; XS: the launch's exponents are known to be in range,
+// else p.exp_safe decides per batch.  The launcher picks the instantiation;
+// the operations on the data are the same in all of them.)
+template <int WPR, int BL, int GM = 0, bool WT = true, int SPL = -1, bool XS = false>
 __global__ void __launch_bounds__(128, BL)
 entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rate,
                   const Edge* __restrict__ adj, const uint32_t* __restrict__ thr,
@@ -180,6 +184,8 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
+    const bool strang = SPL < 0 ? p.strang != 0 : SPL == 1;
+    const bool xsafe = XS || p.exp_safe != 0;
     __shared__ WarpState<RT, CAP> states[4];
     // exp_det's 2^(j/32) table: a shared-memory copy for the 8-block shape
     // (the accumulation batches waited on its L1 lookups: 6.6% of the stall
@@ -243,7 +249,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
 #ifdef EXPMC_CHECKS
             CHK((unsigned long long)__double_as_longlong(q.S[pos]) == kUnfinished);  // parked once
 #endif
-            q.S[pos] = p.strang ? __dsub_rn(S, __dmul_rn(0.5, d)) : S;
+            q.S[pos] = strang ? __dsub_rn(S, __dmul_rn(0.5, d)) : S;
             q.v[pos] = __longlong_as_double((long long)vbits);
             q.tk[tk_slot(pos)].x = jc;
             // (the landing row id, word 0 of the gathered slot, is not needed
@@ -311,7 +317,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
             const double f0 = __dmul_rn(e1, ri.v);
             a.f0 = f0;
             a.K = T0 >= (1ull << 31) ? f0 : 0.0;
-            a.corr = p.strang ? __dmul_rn(0.5, ri.d) : ri.d;
+            a.corr = strang ? __dmul_rn(0.5, ri.d) : ri.d;
         }
         if (tf == tw) {  // the new task is the oldest in flight
             ocl = dead;
@@ -485,7 +491,7 @@ entry_walk_kernel(const RowRec* __restrict__ rec, const double* __restrict__ rat
                 const double x = __dmul_rn(p.dt, __dsub_rn(q.S[pos], m.corr));
                 // (p.exp_safe: |x| <= 690 for every walker of this launch)
                 const double ex = !kTabShared ? exp_det(x)
-                                  : p.exp_safe ? exp_det_inrange(x, s_tab)
+                                  : xsafe ? exp_det_inrange(x, s_tab)
                                                : exp_det_tab(x, s_tab, false);
                 const double dv = __dsub_rn(__dmul_rn(ex, q.v[pos]), m.K);
                 s1 = __dadd_rn(s1, dv);
@@ -734,6 +740,25 @@ int launch_t(const char* name, const DevSplit& m, const uint32_t* rows, uint64_t
 // 4.59 s on config 4); 3 = the pipelined two-set entry_pipe_kernel
 // (walk_entry_short.cuh: bit-identical results, measured slower).
 // Measured, profiles/r02/README.md.
+// The production shape (8 blocks/SM).  An unweighted matrix whose exponents
+// are in range for this launch — every configuration of the benchmark — runs
+// the instantiation with the splitting, the range flag and "no weighted row"
+// fixed at compile time (config 5: 39.29 -> 38.67 ms against the run-time
+// tests); anything else the general one.
+template <int WPR, int GM>
+int launch_shape0(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const FastParams& p,
+                  double* value, double* se, uint64_t* jumps, double4* partial, cudaStream_t s) {
+    if (!m.any_nonuniform && p.exp_safe) {
+        if (p.strang)
+            return launch_t<WPR, entry_walk_kernel<WPR, 8, GM, false, 1, true>, 8>(
+                "entry_walk_kernel", m, rows, nrows, p, value, se, jumps, partial, s);
+        return launch_t<WPR, entry_walk_kernel<WPR, 8, GM, false, 0, true>, 8>(
+            "entry_walk_kernel", m, rows, nrows, p, value, se, jumps, partial, s);
+    }
+    return launch_t<WPR, entry_walk_kernel<WPR, 8, GM>, 8>("entry_walk_kernel", m, rows, nrows, p,
+                                                           value, se, jumps, partial, s);
+}
+
 template <int WPR>
 int launch_w(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const FastParams& p,
              double* value, double* se, uint64_t* jumps, double4* partial, cudaStream_t s) {
@@ -748,18 +773,10 @@ int launch_w(const DevSplit& m, const uint32_t* rows, uint64_t nrows, const Fast
             // random row): ready-ticket look every 16th trip
             // (and enough walkers per task that task slots do not wait on
             // the look: measured 8-20% slower at 16-64 walkers per entry)
-            if (p.beta * m.mean_rate >= ENTRY_LONG_WALK && p.W / WPR >= 512) {
-                if (!m.any_nonuniform)
-                    return launch_t<WPR, entry_walk_kernel<WPR, 8, ENTRY_GATE_MASK, false>, 8>(
-                        "entry_walk_kernel", m, rows, nrows, p, value, se, jumps, partial, s);
-                return launch_t<WPR, entry_walk_kernel<WPR, 8, ENTRY_GATE_MASK>, 8>(
-                    "entry_walk_kernel", m, rows, nrows, p, value, se, jumps, partial, s);
-            }
-            if (!m.any_nonuniform)
-                return launch_t<WPR, entry_walk_kernel<WPR, 8, 0, false>, 8>(
-                    "entry_walk_kernel", m, rows, nrows, p, value, se, jumps, partial, s);
-            return launch_t<WPR, entry_walk_kernel<WPR, 8>, 8>("entry_walk_kernel", m, rows, nrows,
-                                                               p, value, se, jumps, partial, s);
+            if (p.beta * m.mean_rate >= ENTRY_LONG_WALK && p.W / WPR >= 512)
+                return launch_shape0<WPR, ENTRY_GATE_MASK>(m, rows, nrows, p, value, se, jumps,
+                                                           partial, s);
+            return launch_shape0<WPR, 0>(m, rows, nrows, p, value, se, jumps, partial, s);
 #ifdef EXPMC_EXPERIMENTS
         case 5:
             return launch_t<WPR, entry_walk_kernel<WPR, 5>, 5>("entry_walk_kernel", m, rows, nrows,
